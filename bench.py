@@ -1,0 +1,361 @@
+"""Benchmark of the one hot path: FP64 GEMM C = alpha*A*B + beta*C on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload square|rect|large]
+                    [--impl ours|reference] [--no-e2e] [--no-cpu-baseline]
+
+Multi-GPU: torchrun --nproc-per-node N bench.py --gpus N ...  (one process per GPU).
+
+Workloads (BASELINE.json configs):
+  square (default): the metric's N=16384 DGEMM, alpha=1, beta=0, seeded uniform[-1,1).
+          At N GPUs it is WEAK-scaled by rows: each rank owns 16384 rows of
+          A and C (M = 16384*N), B (16384 x 16384) is broadcast from rank 0 over
+          NVLink with NCCL every step (row-block sharding).
+  rect:   config 4, M=32768, N=K=4096 row-sharded over the ranks (strong scaling).
+  large:  config 5, N=65536 square; 8192 rows per rank (weak).
+
+A step = broadcast of B (N>1) + one DGEMM launch over the rank's rows.  Inputs are
+device-resident and larger than L2 (>= 128 MiB each at the default workload), so no
+L2 flush is needed.  Time = CUDA events on the launching stream over exactly K
+steps after W warm-ups, barrier + synchronize on both sides, max over ranks.
+value = 2*M*N*K*K_steps / time (Eq. (4) P:93-97 convention, 2MNK).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "DGEMM TFLOP/s and % of B200 FP64 peak at N=16384 (1 GPU) and 1/2/4/8 GPUs"
+FP64_DATASHEET_TFLOPS = 37.0      # HGX B200: 296 TFLOP/s FP64 / FP64 tensor per 8 GPUs
+BF16_NOMINAL_TFLOPS = 2250.0      # B200_PROFILING.md nominal dense bf16
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="square", choices=["square", "rect", "large"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle sample")
+    ap.add_argument("--cfg", type=int, default=-1, help="force a kernel configuration id")
+    a = ap.parse_args()
+    if a.warmup < 3:
+        a.warmup = 3
+    return a
+
+
+def workload(name, world):
+    """(M_total, N, K, rows_per_rank list, scaling, description)."""
+    if name == "square":
+        n = 16384
+        M = n * world
+        return M, n, n, "weak", f"dgemm_n{n}_rows{n}_per_gpu"
+    if name == "rect":
+        return 32768, 4096, 4096, "strong", "dgemm_m32768_n4096_k4096_rowsharded"
+    n = 65536
+    return 8192 * world, n, n, "weak", f"dgemm_n{n}_rows8192_per_gpu"
+
+
+# ---------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampled every 200 ms during the timed region (B200_PROFILING.md clocks line)."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = str(gpu_index)
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9 and parts[0] == self.idx:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(r[1]) for r in self.rows if num(r[1]) is not None]
+        mx = [num(r[2]) for r in self.rows if num(r[2]) is not None]
+        pw = [num(r[3]) for r in self.rows if num(r[3]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[5 + k].lower().startswith("active")})
+        load = [s for s in sm]   # sampled only inside the timed region
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows),
+                "power_w_median": statistics.median(pw) if pw else None}
+
+
+# ---------------------------------------------------------------------- CPU oracle
+def cpu_oracle_sample(M, N, K, seconds, seed=1706):
+    """Time the CPU oracle (as it stands) on R rows of the workload; returns dict."""
+    import numpy as np
+
+    import oracle
+    import synth
+    threads = oracle.default_threads()
+    B = synth.matrix("uniform", seed, synth.MAT_B, K, N)
+    R = threads
+    A = synth.matrix("uniform", seed, synth.MAT_A, M, K, row0=0, nrows=R)
+    C = np.zeros((R, N))
+    t0 = time.perf_counter()
+    oracle.dgemm(1.0, A, B, 0.0, C, nthreads=threads)
+    dt = time.perf_counter() - t0
+    if dt < seconds / 3:
+        R = max(R, int(R * seconds / max(dt, 1e-3)) // threads * threads)
+        R = min(R, M)
+        A = synth.matrix("uniform", seed, synth.MAT_A, M, K, row0=0, nrows=R)
+        C = np.zeros((R, N))
+        t0 = time.perf_counter()
+        oracle.dgemm(1.0, A, B, 0.0, C, nthreads=threads)
+        dt = time.perf_counter() - t0
+    return {"value": 2.0 * R * N * K / dt / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
+            "sample": f"{R} rows of the {M}x{N}x{K} problem (i-k-j C oracle, -O2, {threads} threads), {dt:.2f} s"}
+
+
+def run_reference(a):
+    """--impl reference: the CPU oracle as it stands, on this arm's config and metric."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import numpy as np
+
+    import oracle
+    import synth
+    world = a.gpus
+    M, N, K, scaling, wname = workload(a.workload, world)
+    threads = oracle.default_threads()
+    B = synth.matrix("uniform", 1706, synth.MAT_B, K, N)
+    R = threads
+    A = synth.matrix("uniform", 1706, synth.MAT_A, M, K, row0=0, nrows=R)
+    C = np.zeros((R, N))
+    for _ in range(a.warmup):
+        oracle.dgemm(1.0, A, B, 0.0, C, nthreads=threads)
+    ts = []
+    for _ in range(a.steps):
+        t0 = time.perf_counter()
+        oracle.dgemm(1.0, A, B, 0.0, C, nthreads=threads)
+        ts.append(time.perf_counter() - t0)
+    tot = sum(ts)
+    value = 2.0 * R * N * K * a.steps / tot / 1e12
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * tot / a.steps, "higher_is_better": True,
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": wname, "M": M, "N": N, "K": K, "alpha": 1.0, "beta": 0.0,
+                       "sample_rows_per_step": R, "parallelism": "host threads"},
+            "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
+                             "sample": f"{R} rows of the {M}x{N}x{K} problem per step (i-k-j C oracle)"},
+            "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------- ours
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1706_10086_b200 import gemm as G
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus:
+        print(f"warning: --gpus {a.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    M, N, K, scaling, wname = workload(a.workload, world)
+    r0, r1 = G.row_range(M, rank, world)
+    Ml = r1 - r0
+    dA = torch.empty((Ml, K), dtype=torch.float64, device="cuda")
+    dB = torch.empty((K, N), dtype=torch.float64, device="cuda")
+    dC = torch.empty((Ml, N), dtype=torch.float64, device="cuda")
+    G.fill(dA, "uniform", 1706, 0, rows=M, row0=r0)
+    if rank == 0:
+        G.fill(dB, "uniform", 1706, 1)
+    else:
+        dB.zero_()
+    G.fill(dC, "uniform", 1706, 2, rows=M, row0=r0)
+    stream = torch.cuda.current_stream()
+    comm = G.Comm(rank, world) if world > 1 else None
+    cfg = a.cfg if a.cfg >= 0 else G.cfg_select(Ml, N, K, dA.data_ptr(), K, dB.data_ptr(), N)
+    cfg_name = G.cfg_name(cfg)
+
+    def step(evs=None):
+        if comm is not None:
+            comm.bcast(dB, root=0, stream=stream)
+        if evs is not None:
+            evs[0].record(stream)
+        G.gemm(dA, dB, dC, 1.0, 0.0, cfg=cfg, stream=stream)
+        if evs is not None:
+            evs[1].record(stream)
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    smi_index = local
+    cvd = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if cvd:
+        try:
+            smi_index = int(cvd.split(",")[local])
+        except (ValueError, IndexError):
+            pass
+    sampler = ClockSampler(smi_index)
+    sampler.start()
+    time.sleep(0.3)
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_start.record(stream)
+    for i in range(a.steps):
+        step(kev[i])
+    e_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.stop()
+    t_ms = e_start.elapsed_time(e_end)
+    k_ms = [s.elapsed_time(e) for s, e in kev]
+    k_mean = statistics.mean(k_ms)
+    if world > 1:
+        t = torch.tensor([t_ms, k_mean], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_ms, k_mean = float(t[0]), float(t[1])
+    flops_step = 2.0 * M * N * K
+    value = flops_step * a.steps / (t_ms * 1e-3) / 1e12
+    flops_local = 2.0 * Ml * N * K
+    achieved = flops_local / (k_mean * 1e-3) / 1e12
+    clocks = sampler.summary()
+
+    # ---- roofline of the dominant (only) kernel ------------------------------------
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        pass
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        pj = json.load(open(prof))
+        key = f"{Ml}x{N}x{K}"
+        if key in pj:
+            traffic = pj[key]["dram_bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
+        pass
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_DATASHEET_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / FP64_DATASHEET_TFLOPS, "traffic": traffic,
+                "kernel": cfg_name, "kernel_ms_mean": k_mean, "flops_per_launch": flops_local,
+                "peak_source": "FP64 / FP64-tensor datasheet peak of one HGX B200 GPU (296/8); MEASURED_PEAKS.json has "
+                               "no FP64 entry (DESIGN.md §Roofline)"}
+    if peaks.get("bf16_tflops"):
+        roofline["peak_bf16_scaled"] = peaks["bf16_tflops"] * FP64_DATASHEET_TFLOPS / BF16_NOMINAL_TFLOPS
+    if clocks.get("sm_mhz"):
+        clk_peak = 148 * 128 * clocks["sm_mhz"] * 1e6 / 1e12
+        roofline["peak_at_run_clock"] = clk_peak
+        roofline["frac_at_run_clock"] = achieved / clk_peak
+
+    # ---- end to end through the host-buffer C-ABI call ------------------------------
+    e2e = None
+    if not a.no_e2e:
+        hA = torch.empty((Ml, K), dtype=torch.float64, pin_memory=True)
+        hB = torch.empty((K, N), dtype=torch.float64, pin_memory=True)
+        hC = torch.empty((Ml, N), dtype=torch.float64, pin_memory=True)
+        hA.copy_(dA)
+        if comm is not None:
+            comm.bcast(dB, root=0, stream=stream)
+        hB.copy_(dB)
+        hC.copy_(dC)
+        del dA, dC
+        torch.cuda.empty_cache()
+        G.gemm_host(hA, hB, hC, 1.0, 0.0)   # warm (allocates the pool)
+        if world > 1:
+            dist.barrier()
+        ts = []
+        for _ in range(a.e2e_steps):
+            t0 = time.perf_counter()
+            G.gemm_host(hA, hB, hC, 1.0, 0.0)
+            ts.append(time.perf_counter() - t0)
+        e2e_s = sum(ts)
+        if world > 1:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t[0])
+        G.host_pool_release()
+        e2e = {"value": flops_step * a.e2e_steps / e2e_s / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": 8 * (M * K + world * K * N), "d2h_bytes_per_step": 8 * M * N,
+               "steps": a.e2e_steps, "api": "gemm_f64_host (pinned host A,B,C; copies overlapped by row panels)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cpu = cpu_oracle_sample(M, N, K, a.cpu_seconds)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": a.steps,
+                "warmup": a.warmup, "ms_per_step": t_ms / a.steps, "higher_is_better": True, "scaling": scaling,
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": wname, "M": M, "N": N, "K": K, "rows_per_gpu": Ml, "alpha": 1.0,
+                           "beta": 0.0, "inputs": "seeded uniform[-1,1) (synth generator, device fill)",
+                           "l2": "inputs larger than L2 (no flush)", "kernel_cfg": cfg_name,
+                           "parallelism": f"row-sharded x{world}, B broadcast (NCCL)" if world > 1 else "1 GPU"},
+                "pct_of_fp64_peak": 100.0 * value / (FP64_DATASHEET_TFLOPS * world),
+                "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": a.steps}
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,188 @@
+/*
+ * gemm_f64.h -- C ABI of the B200-native double-precision GEMM library
+ * (libgemm_f64.so, built from paper_1706_10086_b200/csrc/).
+ *
+ * The one hot path of arXiv 1706.10086 (Matthes et al., "Tuning and
+ * optimization for a variety of many-core architectures without changing a
+ * single line of implementation code using the Alpaka library"):
+ *
+ *     C = alpha * A * B + beta * C                 PAPER.md Eq. (1)
+ *
+ * computed as a tiled GEMM (Fig. 2; §2.1) whose tile size
+ * and elements-per-thread are compile-time parameters (Listing 1).
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ * - Storage is ROW-MAJOR (the paper's inner loop `lineC[j] += a * lineB[j]`,
+ *   Listing 2, walks rows): element (i, j) of an R x S matrix X with
+ *   leading dimension ldX lives at X[i * ldX + j].  A is M x K, B is K x N,
+ *   C is M x N.  Square N x N is the special case M = N = K.
+ * - Matrix pointers are DEVICE pointers (cudaMalloc / torch CUDA tensors) on
+ *   the current device, except in gemm_f64_host().  The caller owns every
+ *   matrix buffer and stream; the library never frees caller memory.
+ * - Calls are asynchronous (enqueue and return, like cuBLAS): launch errors are
+ *   reported through the return code, faults inside a kernel surface at the
+ *   caller's next synchronisation.
+ * - On any argument error NOTHING is enqueued; gemm_last_error() returns a
+ *   thread-local message naming the offending argument.
+ * - Arithmetic: IEEE binary64, round-to-nearest-even, no fast-math.  The sum
+ *   over k is accumulated by the FP64 tensor pipe (mma.sync m8n8k4 f64 ->
+ *   SASS DMMA.8x8x4) in an order different from the oracle's; alpha is applied
+ *   once to the finished sum (reading R5).  Results satisfy,
+ *   elementwise, with u = 2^-53 and mag = |A| |B|:
+ *       |C - C_exact| <= 4 K u |alpha| mag + 4 u |beta| |C0| + 1e-300
+ *   (BASELINE.json north_star).
+ * - BLAS special cases (reading R6):
+ *     M == 0 or N == 0                  -> no-op
+ *     (alpha == 0 or K == 0), beta == 1 -> no-op
+ *     alpha == 0 or K == 0              -> C = beta * C without reading A or B
+ *     beta == 0                         -> C is not read (NaN in C is harmless)
+ * - Argument rules: M, N, K >= 0; lda >= max(1, K); ldb >= max(1, N);
+ *   ldc >= max(1, N); A, B non-NULL when alpha != 0 and K > 0 and M*N > 0;
+ *   C non-NULL when M*N > 0; all pointers 8-byte aligned; C must not overlap
+ *   A or B.  M, N, K < 2^31.
+ *   Pointers 16-byte aligned with even lda/ldb take the TMA path; anything
+ *   else takes a slower GPU path (cp.async staging).  There is no CPU path.
+ */
+#ifndef GEMM_F64_H
+#define GEMM_F64_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define GEMM_API __attribute__((visibility("default")))
+#else
+#define GEMM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    GEMM_OK = 0,
+    GEMM_ERR_ARG = 1,          /* invalid argument (message names it)        */
+    GEMM_ERR_CUDA = 2,         /* CUDA runtime / launch error                */
+    GEMM_ERR_NCCL = 3,         /* NCCL error in a sharded / comm call        */
+    GEMM_ERR_UNSUPPORTED = 4,  /* valid but unsupported (e.g. ldb != N sharded) */
+    GEMM_ERR_ALLOC = 5         /* device or host allocation failed           */
+} gemm_status;
+
+/* ------------------------------------------------------------------ single GPU */
+
+/* C[MxN] = alpha*A[MxK]*B[KxN] + beta*C, row-major, device pointers.
+ * Enqueued on the legacy default stream (stream 0, torch's default stream).
+ * Returns a gemm_status. */
+GEMM_API int gemm_f64(int64_t M, int64_t N, int64_t K, double alpha,
+             const double *A, int64_t lda, const double *B, int64_t ldb,
+             double beta, double *C, int64_t ldc);
+
+/* Same, enqueued on `cuda_stream` (a cudaStream_t; NULL = legacy default). */
+GEMM_API int gemm_f64_stream(int64_t M, int64_t N, int64_t K, double alpha,
+                    const double *A, int64_t lda, const double *B, int64_t ldb,
+                    double beta, double *C, int64_t ldc, void *cuda_stream);
+
+/* Same, forcing kernel configuration `cfg_id` (0 <= cfg_id < gemm_num_cfgs())
+ * instead of the built-in heuristic; cfg_id = -1 means "heuristic".  Used by
+ * the tuning sweep (the paper's "multidimensional parameter tuning").
+ * A TMA configuration given arguments that fail the TMA alignment rules
+ * returns GEMM_ERR_UNSUPPORTED. */
+GEMM_API int gemm_f64_cfg(int64_t M, int64_t N, int64_t K, double alpha,
+                 const double *A, int64_t lda, const double *B, int64_t ldb,
+                 double beta, double *C, int64_t ldc, int cfg_id, void *cuda_stream);
+
+/* Host-buffer entry point ("the call a user makes" with host data): A, B, C are
+ * HOST pointers (pinned for full copy/compute overlap; pageable works but
+ * serialises).  The library allocates device buffers from a cached pool, copies
+ * B and row panels of A (and of C when beta != 0) host->device, computes each
+ * row panel as it lands, and copies result panels device->host while the next
+ * panel computes.  Synchronous: C holds the result when it returns. */
+GEMM_API int gemm_f64_host(int64_t M, int64_t N, int64_t K, double alpha,
+                  const double *A, int64_t lda, const double *B, int64_t ldb,
+                  double beta, double *C, int64_t ldc);
+
+/* Release the device buffers cached by gemm_f64_host on the current device. */
+GEMM_API int gemm_host_pool_release(void);
+
+/* ------------------------------------------------------------ configurations */
+
+typedef struct {
+    int bm, bn, bk;     /* CTA tile of C (BM x BN) and k-depth per pipeline stage */
+    int wm, wn;         /* warp tile; elements (accumulators) per thread = wm*wn/32 */
+    int stages;         /* shared-memory pipeline depth                            */
+    int threads;        /* threads per CTA (lane 0 of warp 0 doubles as TMA producer) */
+    int smem_bytes;     /* dynamic shared memory per CTA                           */
+    int tma;            /* 1: TMA + mbarrier pipeline; 0: cp.async staging          */
+    int split_k;        /* >1: deterministic split-K kernel family                */
+    int regs;           /* registers per thread (from cudaFuncGetAttributes; 0 before first use) */
+} gemm_cfg_desc;
+
+GEMM_API int gemm_num_cfgs(void);
+/* Writes a NUL-terminated name such as "tma_128x128x16_w64x32_s4" into buf. */
+GEMM_API int gemm_cfg_name(int cfg_id, char *buf, int len);
+GEMM_API int gemm_cfg_info(int cfg_id, gemm_cfg_desc *out);
+/* The configuration the heuristic picks for this shape / alignment. */
+GEMM_API int gemm_cfg_select(int64_t M, int64_t N, int64_t K, const double *A, int64_t lda,
+                    const double *B, int64_t ldb);
+
+/* Thread-local message for the last non-OK return on this thread. */
+GEMM_API const char *gemm_last_error(void);
+
+/* -------------------------------------------------------- synthetic inputs */
+
+/* Fills rows [row0, row0+nrows) of a logical rows x cols matrix into
+ * X (device, row-major, leading dimension ldx; X points at logical row row0)
+ * with the counter-based generator documented in synth/__init__.py:
+ * mode 0 uniform[-1,1), 1 dyadic m/256, 2 integers [-8,8], 3 ones,
+ * 4 identity, 5 zeros; mat = matrix id (A=0, B=1, C0=2).  Bitwise identical
+ * to synth.matrix() (tested).  Input synthesis only -- no GEMM arithmetic. */
+GEMM_API int gemm_fill_f64(int mode, uint64_t seed, int mat, int64_t rows, int64_t cols,
+                  int64_t row0, int64_t nrows, double *X, int64_t ldx, void *cuda_stream);
+
+/* ------------------------------------------------- FP64 peak microbenchmarks */
+
+/* Launches `blocks` x (32*warps) threads; each warp issues `iters` rounds of
+ * 8 independent mma.m8n8k4.f64 (DMMA.8x8x4, 512 FLOP each) or, with
+ * kind = 1, each thread issues `iters` rounds of 8 independent DFMA.
+ * Writes one double per block to out[blocks] (to defeat dead-code removal) and
+ * the SM cycle count of block 0 to cycles_out[0] (device int64).
+ * FLOPs issued = blocks*warps*iters*8*512 (DMMA) or blocks*warps*32*iters*8*2 (DFMA). */
+GEMM_API int gemm_peak_probe(int kind, int blocks, int warps, int64_t iters,
+                    double *out, int64_t *cycles_out, void *cuda_stream);
+
+/* --------------------------------------------------- multi-GPU (one process per GPU) */
+
+/* Rank 0 creates the 128-byte NCCL unique id; distribute it to all ranks
+ * (e.g. with torch.distributed.broadcast) before gemm_comm_init. */
+GEMM_API int gemm_comm_unique_id(unsigned char id_out[128]);
+/* Creates the library-owned communicator for `rank` of `nranks` on the current
+ * device.  *comm_out receives an opaque handle. */
+GEMM_API int gemm_comm_init(void **comm_out, int nranks, const unsigned char id[128], int rank);
+GEMM_API int gemm_comm_destroy(void *comm);
+
+/* Row-block-sharded GEMM (collective: every rank calls it with the same N, K,
+ * alpha, beta, root).  Rank r owns rows [floor(r*M/P), floor((r+1)*M/P)) of A
+ * and C (M_local of them; may differ between ranks).  B (K x N, contiguous,
+ * ldb == N required else GEMM_ERR_UNSUPPORTED) is the source on `root` and a
+ * receive buffer (overwritten) elsewhere; it is broadcast over NVLink with
+ * NCCL, in `bcast_chunks` column panels (>= 1) so that panel j+1 travels while
+ * panel j is multiplied -- per-entry arithmetic is unchanged, so the result is
+ * bitwise equal to the single-GPU call with the same configuration.
+ * Then each rank computes C_local = alpha*A_local*B + beta*C_local. */
+GEMM_API int gemm_f64_sharded(int64_t M_local, int64_t N, int64_t K, double alpha,
+                     const double *A_local, int64_t lda, double *B, int64_t ldb,
+                     double beta, double *C_local, int64_t ldc,
+                     void *comm, int root, int bcast_chunks, void *cuda_stream);
+
+/* Plain broadcast of a device buffer of `count` doubles (exposed for tests and
+ * for timing the exchange step alone). */
+GEMM_API int gemm_bcast_f64(double *buf, int64_t count, int root, void *comm, void *cuda_stream);
+
+/* Library version string. */
+GEMM_API const char *gemm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GEMM_F64_H */

@@ -1,0 +1,360 @@
+// dgemm_kernels.cuh -- sm_100a FP64 GEMM kernels: C = alpha*A*B + beta*C, row-major.
+//
+// PAPER.md Eq. (1); tiled algorithm Fig. 2 P:102-107 and §2.1 P:131-133:
+// "calculate one tile of the matrix C per Alpaka block ... Every element stores
+// the partial result of alpha*A*B in element local memory".  The paper's tunables
+// (tile size T and elements per thread, Listing 1) become the
+// compile-time tile parameters of Cfg below:
+//
+//   BM x BN   CTA tile of C            (the paper's block tile t*T)
+//   BK        k-depth of one pipeline stage (multiple of 16)
+//   WM x WN   warp tile; E = WM*WN/32 accumulators per thread
+//             (the paper's "elements per thread", its element layer)
+//   STAGES    depth of the shared-memory ring (the paper's A/B tile cache, Eq. (5))
+//
+// B200 design:
+// * a1 work division: one CTA per BM x BN tile of C, grouped ("swizzled") raster of
+//   group_m tile rows so that CTAs resident together share A and B panels in L2.
+// * a2 staging: A tile (BM x 16 doubles per k-group, 128-byte rows) and B tile
+//   (16 x 16-double boxes) land in shared memory through TMA with the 128-byte
+//   swizzle (16-byte chunk index ^= row & 7), driven by one producer warp and a
+//   ring of full/empty mbarriers (tma kernel), or through cp.async into the same
+//   swizzled layout (generic kernel, any alignment / leading dimension).
+// * a3 tile MMA: mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4, the only native FP64 MMA of
+//   sm_100a; tcgen05 has no f64 kind).  Fragments are read with 16-byte LDS through
+//   a k-permutation chosen so that, under the TMA 128-byte swizzle, both the A and
+//   the B fragment loads are free of bank conflicts (see kperm_chunk below).
+// * a4 epilogue: alpha once on the finished sum, beta*C read only when beta != 0,
+//   4 contiguous doubles per thread -> one 256-bit STG per (m-block, n-pair).
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+
+#include "ptx.cuh"
+
+namespace dg {
+
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_>
+struct Cfg {
+    static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_;
+    static_assert(BM % WM == 0 && BN % WN == 0, "warp tiles must tile the CTA tile");
+    static_assert(WM % 8 == 0 && WN % 16 == 0, "warp tile: m-blocks of 8, n-pairs of 16");
+    static_assert(BK % 16 == 0, "BK is a multiple of the 16-wide k-permutation group");
+    static_assert(BM <= 256, "TMA box rows <= 256");
+    static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
+    static constexpr int CONSUMER_WARPS = WARPS_M * WARPS_N;
+    static constexpr int CONSUMER_THREADS = CONSUMER_WARPS * 32;
+    static constexpr int MB = WM / 8;    // 8-row m-blocks per warp
+    static constexpr int NP = WN / 16;   // 16-column n-pairs per warp (two 8-wide n-blocks each)
+    static constexpr int KG = BK / 16;   // 16-deep k-groups per stage
+    static constexpr int E = WM * WN / 32;
+    // shared-memory layout of one stage: A sub-tiles [KG][BM][16], then B boxes [KG][BN/16][16][16]
+    static constexpr uint32_t A_SUB = BM * 128;
+    static constexpr uint32_t A_BYTES = KG * A_SUB;
+    static constexpr uint32_t B_BOX = 16 * 128;
+    static constexpr uint32_t B_KG = (BN / 16) * B_BOX;
+    static constexpr uint32_t B_BYTES = KG * B_KG;
+    static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr uint32_t BAR_BYTES = 2 * STAGES * 8;
+    static constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + BAR_BYTES + 1024;  // +1024: manual alignment
+};
+
+// k-permutation inside a 16-deep k-group.  A thread with MMA k-index t (= lane & 3)
+// and half p in {0,1} owns the 16-byte chunk c(t,p) (two consecutive k) of each
+// 128-byte row; MMA slice q = 2p+s uses real k = 2*c(t,p) + s.  (t,p) -> c is a
+// bijection onto 0..7, so every k of the group is used exactly once per slice set.
+// With the hardware 128-byte swizzle (physical chunk = chunk ^ (row & 7)):
+//  * A loads (rows g = lane>>2, chunk c(t,p)) hit 8 distinct chunks per 8-lane phase
+//    because c(t,p) >> 1 is distinct over t;
+//  * B loads (row k = 2c+s, chunk g) hit 8 distinct chunks per phase because
+//    c(t,p) & 3 is distinct over t.
+__device__ __forceinline__ int kperm_chunk(int t, int p) { return t + 4 * ((t & 1) ^ p); }
+
+__device__ __forceinline__ void lds_v2(uint32_t addr, double &x, double &y) {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(x), "=d"(y) : "r"(addr));
+}
+
+// Per-thread constant offsets for fragment loads.
+template <class C>
+struct FragOffsets {
+    uint32_t a[2];      // A: byte offset within a k-group sub-tile, for p = 0, 1 (includes warp row)
+    uint32_t b[2][2];   // B: byte offset within a k-group, for (p, s) (includes warp n-pair base)
+    __device__ __forceinline__ FragOffsets(int warp_m, int warp_n, int lane) {
+        const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            const int c = kperm_chunk(t, p);
+            a[p] = (uint32_t)((warp_m * C::WM + g) * 128 + ((c ^ g) << 4));
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+                const int k = 2 * c + s;
+                b[p][s] = (uint32_t)((warp_n * C::WN / 16) * C::B_BOX + k * 128 + ((g ^ (k & 7)) << 4));
+            }
+        }
+    }
+};
+
+// One pipeline stage of the warp's register-blocked tile multiply (row a3).
+template <class C>
+__device__ __forceinline__ void mma_stage(uint32_t sA, uint32_t sB, const FragOffsets<C> &fo,
+                                          double (&acc)[C::MB][C::NP][2][2]) {
+#pragma unroll
+    for (int kg = 0; kg < C::KG; ++kg) {
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            double a[C::MB][2];
+            double b[C::NP][2][2];
+#pragma unroll
+            for (int mb = 0; mb < C::MB; ++mb)
+                lds_v2(sA + kg * C::A_SUB + mb * 1024 + fo.a[p], a[mb][0], a[mb][1]);
+#pragma unroll
+            for (int np = 0; np < C::NP; ++np)
+#pragma unroll
+                for (int s = 0; s < 2; ++s)
+                    lds_v2(sB + kg * C::B_KG + np * C::B_BOX + fo.b[p][s], b[np][s][0], b[np][s][1]);
+#pragma unroll
+            for (int s = 0; s < 2; ++s)
+#pragma unroll
+                for (int mb = 0; mb < C::MB; ++mb)
+#pragma unroll
+                    for (int np = 0; np < C::NP; ++np)
+#pragma unroll
+                        for (int j = 0; j < 2; ++j)
+                            dmma_m8n8k4(acc[mb][np][j][0], acc[mb][np][j][1], a[mb][s], b[np][s][j]);
+        }
+    }
+}
+
+// Epilogue (row a4): C = alpha*acc + beta*C, each C element read (beta != 0) and written once.
+// Thread (g, t) of an (m-block, n-pair) owns row g and the 4 contiguous columns 4t..4t+3:
+// acc[mb][np][j][i] is real column 4t + 2i + j of the n-pair.
+template <class C>
+__device__ __forceinline__ void epilogue(const double (&acc)[C::MB][C::NP][2][2], int row0, int col0, int lane,
+                                         int M, int N, double alpha, double beta, double *__restrict__ Cm,
+                                         int64_t ldc, bool vec) {
+    const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+    for (int mb = 0; mb < C::MB; ++mb) {
+        const int row = row0 + mb * 8 + g;
+        if (row >= M) continue;
+        double *crow = Cm + (int64_t)row * ldc;
+#pragma unroll
+        for (int np = 0; np < C::NP; ++np) {
+            const int col = col0 + np * 16 + 4 * t;
+            double v[4] = {acc[mb][np][0][0], acc[mb][np][1][0], acc[mb][np][0][1], acc[mb][np][1][1]};
+            if (vec && col + 3 < N) {
+                double o[4];
+                if (beta != 0.0) {
+                    double c[4];
+                    ldg_v4(crow + col, c[0], c[1], c[2], c[3]);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) o[e] = fma(alpha, v[e], beta * c[e]);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) o[e] = alpha * v[e];
+                }
+                stg_v4(crow + col, o[0], o[1], o[2], o[3]);
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    if (col + e < N) {
+                        const double o = (beta != 0.0) ? fma(alpha, v[e], beta * crow[col + e]) : alpha * v[e];
+                        crow[col + e] = o;
+                    }
+                }
+            }
+        }
+    }
+}
+
+// Grouped raster (row a1): consecutive CTAs walk group_m tile-rows column by column.
+__device__ __forceinline__ void tile_coords(int bid, int tiles_m, int tiles_n, int group_m, int &tm, int &tn) {
+    const int per_group = group_m * tiles_n;
+    const int group = bid / per_group;
+    const int first_m = group * group_m;
+    const int gsize = min(group_m, tiles_m - first_m);
+    const int r = bid - group * per_group;
+    tm = first_m + r % gsize;
+    tn = r / gsize;
+}
+
+// ------------------------------------------------------------------------------
+// TMA + mbarrier kernel.  No dedicated producer warp: a separate warp would push
+// the per-SMSP warp count from 2 to 3 and cap registers at 168/thread (the 64x32
+// warp tile needs ~200).  Lane 0 of warp 0 is the producer: at the top of k-step kt
+// it waits until every consumer warp has released the slot read at kt-1 (empty
+// mbarrier) and refills it with k-step kt-1+STAGES by TMA (full mbarrier,
+// expect_tx).  STAGES-1 stages stay in flight ahead of the slowest warp.
+template <class C>
+__device__ __forceinline__ void tma_issue_stage(uint8_t *stage_ptr, const CUtensorMap *tmA, const CUtensorMap *tmB,
+                                                uint64_t *full_bar, int m0, int n0, int kt, uint64_t pol) {
+    mbar_arrive_expect_tx(full_bar, C::STAGE_BYTES);
+    uint8_t *sA = stage_ptr;
+    uint8_t *sB = stage_ptr + C::A_BYTES;
+#pragma unroll
+    for (int kg = 0; kg < C::KG; ++kg) {
+        const int k = kt * C::BK + kg * 16;
+        tma_load_2d(sA + kg * C::A_SUB, tmA, k, m0, full_bar, pol);
+#pragma unroll
+        for (int c = 0; c < C::BN / 16; ++c)
+            tma_load_2d(sB + kg * C::B_KG + c * C::B_BOX, tmB, n0 + 16 * c, k, full_bar, pol);
+    }
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::CONSUMER_THREADS, 1)
+    dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
+                     int N, int K, double alpha, double beta, double *__restrict__ Cm, int64_t ldc, int vec,
+                     int group_m) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t *base_ptr = smem_raw + (base - raw);
+    uint64_t *full = reinterpret_cast<uint64_t *>(base_ptr + C::STAGES * C::STAGE_BYTES);
+    uint64_t *empty = full + C::STAGES;
+
+    const int tiles_m = (M + C::BM - 1) / C::BM, tiles_n = (N + C::BN - 1) / C::BN;
+    int tm, tn;
+    tile_coords(blockIdx.x, tiles_m, tiles_n, group_m, tm, tn);
+    const int m0 = tm * C::BM, n0 = tn * C::BN;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int KT = (K + C::BK - 1) / C::BK;
+    const bool producer = (threadIdx.x == 0);
+    uint64_t pol = 0;
+
+    if (producer) {
+#pragma unroll
+        for (int s = 0; s < C::STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], C::CONSUMER_WARPS);
+        }
+        fence_mbar_init();
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+        pol = l2_policy_evict_normal();
+        for (int s = 0; s < C::STAGES && s < KT; ++s)
+            tma_issue_stage<C>(base_ptr + s * C::STAGE_BYTES, &tmA, &tmB, &full[s], m0, n0, s, pol);
+    }
+    __syncthreads();
+
+    const int warp_m = warp / C::WARPS_N, warp_n = warp % C::WARPS_N;
+    const FragOffsets<C> fo(warp_m, warp_n, lane);
+    double acc[C::MB][C::NP][2][2];
+#pragma unroll
+    for (int mb = 0; mb < C::MB; ++mb)
+#pragma unroll
+        for (int np = 0; np < C::NP; ++np)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) acc[mb][np][j][0] = acc[mb][np][j][1] = 0.0;
+
+    for (int kt = 0; kt < KT; ++kt) {
+        const int s = kt % C::STAGES;
+        if (producer && kt > 0) {
+            const int kn = kt - 1 + C::STAGES;   // refill the slot released at kt-1
+            if (kn < KT) {
+                const int sp = (kt - 1) % C::STAGES;
+                mbar_wait(&empty[sp], ((kt - 1) / C::STAGES) & 1);
+                tma_issue_stage<C>(base_ptr + sp * C::STAGE_BYTES, &tmA, &tmB, &full[sp], m0, n0, kn, pol);
+            }
+        }
+        mbar_wait(&full[s], (kt / C::STAGES) & 1);
+        const uint32_t sA = base + s * C::STAGE_BYTES;
+        mma_stage<C>(sA, sA + C::A_BYTES, fo, acc);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    epilogue<C>(acc, m0 + warp_m * C::WM, n0 + warp_n * C::WN, lane, M, N, alpha, beta, Cm, ldc, vec != 0);
+}
+
+// ------------------------------------------------------------------------------
+// Generic kernel: any 8-byte-aligned pointers and leading dimensions.  All warps
+// stage tiles with 8-byte cp.async (zero-filled outside the matrix) into the same
+// swizzled layout, STAGES-deep ring with cp.async groups.
+template <class C>
+__device__ __forceinline__ void generic_load_stage(uint32_t sA, uint32_t sB, const double *__restrict__ A,
+                                                   int64_t lda, const double *__restrict__ B, int64_t ldb,
+                                                   int M, int N, int K, int m0, int n0, int k0) {
+    const int tid = threadIdx.x;
+    for (int idx = tid; idx < C::BM * C::BK; idx += C::CONSUMER_THREADS) {
+        const int r = idx / C::BK, k = idx % C::BK;
+        const int gm = m0 + r, gk = k0 + k;
+        const bool ok = gm < M && gk < K;
+        const double *src = ok ? A + (int64_t)gm * lda + gk : A;
+        const uint32_t dst = sA + (k >> 4) * C::A_SUB + r * 128 + ((((k & 15) >> 1) ^ (r & 7)) << 4) + (k & 1) * 8;
+        cp_async_8(dst, src, ok);
+    }
+    for (int idx = tid; idx < C::BK * C::BN; idx += C::CONSUMER_THREADS) {
+        const int k = idx / C::BN, n = idx % C::BN;
+        const int gk = k0 + k, gn = n0 + n;
+        const bool ok = gk < K && gn < N;
+        const double *src = ok ? B + (int64_t)gk * ldb + gn : B;
+        const int kk = k & 15, nn = n & 15;
+        const uint32_t dst = sB + (k >> 4) * C::B_KG + (n >> 4) * C::B_BOX + kk * 128 +
+                             ((((nn >> 1) ^ (kk & 7))) << 4) + (nn & 1) * 8;
+        cp_async_8(dst, src, ok);
+    }
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::CONSUMER_THREADS, 1)
+    dgemm_generic_kernel(const double *__restrict__ A, int64_t lda, const double *__restrict__ B, int64_t ldb,
+                         int M, int N, int K, double alpha, double beta, double *__restrict__ Cm, int64_t ldc,
+                         int vec, int group_m) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+
+    const int tiles_m = (M + C::BM - 1) / C::BM, tiles_n = (N + C::BN - 1) / C::BN;
+    int tm, tn;
+    tile_coords(blockIdx.x, tiles_m, tiles_n, group_m, tm, tn);
+    const int m0 = tm * C::BM, n0 = tn * C::BN;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int KT = (K + C::BK - 1) / C::BK;
+
+#pragma unroll
+    for (int s = 0; s < C::STAGES - 1; ++s) {
+        if (s < KT) {
+            const uint32_t sA = base + s * C::STAGE_BYTES;
+            generic_load_stage<C>(sA, sA + C::A_BYTES, A, lda, B, ldb, M, N, K, m0, n0, s * C::BK);
+        }
+        cp_async_commit();
+    }
+
+    const int warp_m = warp / C::WARPS_N, warp_n = warp % C::WARPS_N;
+    const FragOffsets<C> fo(warp_m, warp_n, lane);
+    double acc[C::MB][C::NP][2][2];
+#pragma unroll
+    for (int mb = 0; mb < C::MB; ++mb)
+#pragma unroll
+        for (int np = 0; np < C::NP; ++np)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) acc[mb][np][j][0] = acc[mb][np][j][1] = 0.0;
+
+    for (int kt = 0; kt < KT; ++kt) {
+        cp_async_wait<C::STAGES - 2>();
+        __syncthreads();
+        const int kn = kt + C::STAGES - 1;
+        if (kn < KT) {
+            const uint32_t sA = base + (kn % C::STAGES) * C::STAGE_BYTES;
+            generic_load_stage<C>(sA, sA + C::A_BYTES, A, lda, B, ldb, M, N, K, m0, n0, kn * C::BK);
+        }
+        cp_async_commit();
+        const uint32_t sA = base + (kt % C::STAGES) * C::STAGE_BYTES;
+        mma_stage<C>(sA, sA + C::A_BYTES, fo, acc);
+    }
+    cp_async_wait<0>();
+    epilogue<C>(acc, m0 + warp_m * C::WM, n0 + warp_n * C::WN, lane, M, N, alpha, beta, Cm, ldc, vec != 0);
+}
+
+// C = beta*C (alpha == 0 or K == 0); beta == 0 writes zeros without reading C.
+__global__ void scale_kernel(int M, int N, double beta, double *__restrict__ Cm, int64_t ldc) {
+    const int64_t total = (int64_t)M * N;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = idx / N, j = idx % N;
+        double *p = Cm + i * ldc + j;
+        *p = (beta == 0.0) ? 0.0 : beta * *p;
+    }
+}
+
+}  // namespace dg

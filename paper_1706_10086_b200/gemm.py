@@ -1,0 +1,277 @@
+"""Thin ctypes binding of libgemm_f64.so (include/gemm_f64.h).
+
+Argument marshalling only: every step of C = alpha*A*B + beta*C (PAPER.md
+Eq. (1)) runs in the CUDA kernels behind the C ABI.  PyTorch is used
+for device memory and streams.  There is no fallback: if the library is
+missing or fails to load, importing this module raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgemm_f64.so")
+
+GEMM_OK, GEMM_ERR_ARG, GEMM_ERR_CUDA, GEMM_ERR_NCCL, GEMM_ERR_UNSUPPORTED, GEMM_ERR_ALLOC = range(6)
+STATUS_NAMES = {0: "GEMM_OK", 1: "GEMM_ERR_ARG", 2: "GEMM_ERR_CUDA", 3: "GEMM_ERR_NCCL",
+                4: "GEMM_ERR_UNSUPPORTED", 5: "GEMM_ERR_ALLOC"}
+FILL_MODES = {"uniform": 0, "dyadic": 1, "int8": 2, "ones": 3, "identity": 4, "zeros": 5}
+
+# every symbol include/gemm_f64.h declares (tests check the library exports them all)
+EXPORTS = ("gemm_f64", "gemm_f64_stream", "gemm_f64_cfg", "gemm_f64_host", "gemm_host_pool_release",
+           "gemm_num_cfgs", "gemm_cfg_name", "gemm_cfg_info", "gemm_cfg_select", "gemm_last_error",
+           "gemm_fill_f64", "gemm_peak_probe", "gemm_comm_unique_id", "gemm_comm_init",
+           "gemm_comm_destroy", "gemm_f64_sharded", "gemm_bcast_f64", "gemm_version")
+
+
+class GemmError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class CfgDesc(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int) for n in
+                ("bm", "bn", "bk", "wm", "wn", "stages", "threads", "smem_bytes", "tma", "split_k", "regs")]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_1706_10086_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    i64, dbl, vp, ci = ctypes.c_int64, ctypes.c_double, ctypes.c_void_p, ctypes.c_int
+    core = [i64, i64, i64, dbl, vp, i64, vp, i64, dbl, vp, i64]
+    sig = {
+        "gemm_f64": (ci, core),
+        "gemm_f64_stream": (ci, core + [vp]),
+        "gemm_f64_cfg": (ci, core + [ci, vp]),
+        "gemm_f64_host": (ci, core),
+        "gemm_host_pool_release": (ci, []),
+        "gemm_num_cfgs": (ci, []),
+        "gemm_cfg_name": (ci, [ci, ctypes.c_char_p, ci]),
+        "gemm_cfg_info": (ci, [ci, ctypes.POINTER(CfgDesc)]),
+        "gemm_cfg_select": (ci, [i64, i64, i64, vp, i64, vp, i64]),
+        "gemm_last_error": (ctypes.c_char_p, []),
+        "gemm_fill_f64": (ci, [ci, ctypes.c_uint64, ci, i64, i64, i64, i64, vp, i64, vp]),
+        "gemm_peak_probe": (ci, [ci, ci, ci, i64, vp, vp, vp]),
+        "gemm_comm_unique_id": (ci, [ctypes.c_char_p]),
+        "gemm_comm_init": (ci, [ctypes.POINTER(vp), ci, ctypes.c_char_p, ci]),
+        "gemm_comm_destroy": (ci, [vp]),
+        "gemm_f64_sharded": (ci, [i64, i64, i64, dbl, vp, i64, vp, i64, dbl, vp, i64, vp, ci, ci, vp]),
+        "gemm_bcast_f64": (ci, [vp, i64, ci, vp, vp]),
+        "gemm_version": (ctypes.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+_lib = _load()
+
+
+def lib():
+    return _lib
+
+
+def last_error() -> str:
+    return _lib.gemm_last_error().decode()
+
+
+def version() -> str:
+    return _lib.gemm_version().decode()
+
+
+def _check(rc: int):
+    if rc != GEMM_OK:
+        raise GemmError(rc, last_error())
+
+
+# ------------------------------------------------------------------ tensors
+def _mat(x, name):
+    """(ptr, rows, cols, ld) of a 2-D float64 tensor with unit column stride."""
+    if x.dtype.__str__() not in ("torch.float64", "float64"):
+        raise TypeError(f"{name} must be float64, got {x.dtype}")
+    if x.dim() != 2:
+        raise ValueError(f"{name} must be 2-D")
+    r, c = x.shape
+    if x.numel() == 0:
+        return x.data_ptr(), r, c, max(c, 1)
+    if c > 1 and x.stride(1) != 1:
+        raise ValueError(f"{name} must have unit stride along columns (row-major)")
+    ld = x.stride(0) if r > 1 else max(1, c)
+    ld = max(ld, c, 1)
+    return x.data_ptr(), r, c, ld
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def gemm(A, B, C, alpha: float = 1.0, beta: float = 0.0, cfg: int | None = None, stream=None):
+    """C <- alpha*A@B + beta*C on the GPU (torch CUDA float64 tensors, row-major). Returns C."""
+    pa, M, K, lda = _mat(A, "A")
+    pb, K2, N, ldb = _mat(B, "B")
+    pc, M2, N2, ldc = _mat(C, "C")
+    if K2 != K or M2 != M or N2 != N:
+        raise ValueError(f"shape mismatch A{tuple(A.shape)} B{tuple(B.shape)} C{tuple(C.shape)}")
+    for t, n in ((A, "A"), (B, "B"), (C, "C")):
+        if not t.is_cuda:
+            raise ValueError(f"{n} must be a CUDA tensor (use gemm_host for host buffers)")
+    st = _stream_ptr(stream)
+    if cfg is None:
+        rc = _lib.gemm_f64_stream(M, N, K, float(alpha), pa, lda, pb, ldb, float(beta), pc, ldc, st)
+    else:
+        rc = _lib.gemm_f64_cfg(M, N, K, float(alpha), pa, lda, pb, ldb, float(beta), pc, ldc, int(cfg), st)
+    _check(rc)
+    return C
+
+
+def gemm_raw(M, N, K, alpha, A_ptr, lda, B_ptr, ldb, beta, C_ptr, ldc, cfg=-1, stream=0) -> int:
+    """Raw C-ABI call with integer device pointers; returns the status code (no raise)."""
+    return _lib.gemm_f64_cfg(int(M), int(N), int(K), float(alpha), A_ptr, int(lda), B_ptr, int(ldb),
+                             float(beta), C_ptr, int(ldc), int(cfg), stream)
+
+
+def gemm_host(A, B, C, alpha: float = 1.0, beta: float = 0.0):
+    """C <- alpha*A@B + beta*C with HOST buffers (numpy arrays or CPU torch tensors)."""
+    def info(x, name):
+        if hasattr(x, "data_ptr"):
+            return _mat(x, name)
+        import numpy as np
+        if x.dtype != np.float64 or x.ndim != 2 or (x.shape[1] > 1 and x.strides[1] != 8):
+            raise ValueError(f"{name} must be a row-major float64 2-D array")
+        r, c = x.shape
+        ld = max(x.strides[0] // 8 if r > 1 else c, c, 1)
+        return x.ctypes.data, r, c, ld
+    pa, M, K, lda = info(A, "A")
+    pb, K2, N, ldb = info(B, "B")
+    pc, M2, N2, ldc = info(C, "C")
+    if K2 != K or M2 != M or N2 != N:
+        raise ValueError("shape mismatch")
+    _check(_lib.gemm_f64_host(M, N, K, float(alpha), pa, lda, pb, ldb, float(beta), pc, ldc))
+    return C
+
+
+def host_pool_release():
+    _check(_lib.gemm_host_pool_release())
+
+
+# ------------------------------------------------------------------ configs
+def num_cfgs() -> int:
+    return _lib.gemm_num_cfgs()
+
+
+def cfg_name(i: int) -> str:
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.gemm_cfg_name(i, buf, 128))
+    return buf.value.decode()
+
+
+def cfg_info(i: int) -> dict:
+    d = CfgDesc()
+    _check(_lib.gemm_cfg_info(i, ctypes.byref(d)))
+    out = {n: getattr(d, n) for n, _ in CfgDesc._fields_}
+    out["name"] = cfg_name(i)
+    out["id"] = i
+    out["e"] = out["wm"] * out["wn"] // 32
+    return out
+
+
+def cfgs() -> list:
+    return [cfg_info(i) for i in range(num_cfgs())]
+
+
+def cfg_id(name: str) -> int:
+    for i in range(num_cfgs()):
+        if cfg_name(i) == name:
+            return i
+    raise KeyError(name)
+
+
+def cfg_select(M, N, K, A_ptr=0, lda=None, B_ptr=0, ldb=None) -> int:
+    return _lib.gemm_cfg_select(M, N, K, A_ptr, lda if lda is not None else max(K, 1), B_ptr,
+                                ldb if ldb is not None else max(N, 1))
+
+
+# ------------------------------------------------------------------ inputs
+def fill(X, mode: str, seed: int, mat: int, rows: int | None = None, row0: int = 0, stream=None):
+    """Fill device tensor X (nrows x cols) with rows [row0, row0+nrows) of the logical
+    rows x cols matrix of synth's counter-based generator (bitwise identical)."""
+    px, nrows, cols, ldx = _mat(X, "X")
+    if rows is None:
+        rows = row0 + nrows
+    _check(_lib.gemm_fill_f64(FILL_MODES[mode], int(seed) & (2 ** 64 - 1), int(mat), int(rows), int(cols),
+                              int(row0), int(nrows), px, ldx, _stream_ptr(stream)))
+    return X
+
+
+def peak_probe(kind: str, blocks: int, warps: int, iters: int, out, cycles=None, stream=None):
+    k = {"dmma": 0, "dfma": 1}[kind]
+    _check(_lib.gemm_peak_probe(k, blocks, warps, iters, out.data_ptr(),
+                                cycles.data_ptr() if cycles is not None else None, _stream_ptr(stream)))
+
+
+# ------------------------------------------------------------------ multi-GPU
+class Comm:
+    """Library-owned NCCL communicator (one process per GPU).  The 128-byte id is
+    created on rank 0 and distributed with torch.distributed (any backend)."""
+
+    def __init__(self, rank: int, world: int, group=None):
+        import torch
+        import torch.distributed as dist
+        idbuf = ctypes.create_string_buffer(128)
+        if rank == 0:
+            _check(_lib.gemm_comm_unique_id(idbuf))
+        payload = [bytes(idbuf.raw)] if rank == 0 else [None]
+        if world > 1:
+            dist.broadcast_object_list(payload, src=0, group=group)
+        raw = payload[0]
+        self._h = ctypes.c_void_p()
+        _check(_lib.gemm_comm_init(ctypes.byref(self._h), world, ctypes.create_string_buffer(raw, 128), rank))
+        self.rank, self.world = rank, world
+        self._torch = torch
+
+    @property
+    def handle(self):
+        return self._h
+
+    def bcast(self, X, root: int = 0, stream=None):
+        _check(_lib.gemm_bcast_f64(X.data_ptr(), X.numel(), root, self._h, _stream_ptr(stream)))
+
+    def gemm_sharded(self, A_local, B, C_local, alpha=1.0, beta=0.0, root=0, bcast_chunks=1, stream=None):
+        pa, M, K, lda = _mat(A_local, "A_local")
+        pb, K2, N, ldb = _mat(B, "B")
+        pc, M2, N2, ldc = _mat(C_local, "C_local")
+        if K2 != K or M2 != M or N2 != N:
+            raise ValueError("shape mismatch")
+        _check(_lib.gemm_f64_sharded(M, N, K, float(alpha), pa, lda, pb, ldb, float(beta), pc, ldc,
+                                     self._h, int(root), int(bcast_chunks), _stream_ptr(stream)))
+        return C_local
+
+    def close(self):
+        if self._h:
+            _check(_lib.gemm_comm_destroy(self._h))
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def row_range(M: int, rank: int, world: int) -> tuple:
+    """Rows [floor(r*M/P), floor((r+1)*M/P)) owned by `rank` (include/gemm_f64.h sharded contract)."""
+    if world < 1 or not (0 <= rank < world) or M < 0:
+        raise ValueError(f"bad partition M={M} rank={rank} world={world}")
+    return (rank * M) // world, ((rank + 1) * M) // world

@@ -1,0 +1,327 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar: elementwise
+    |C_gpu - C_ref| <= 4 K 2^-53 |alpha| (|A||B|)_ij + 4 2^-53 |beta| |C0_ij| + 1e-300
+on seeded uniform[-1,1) inputs (BASELINE.json north_star); BITWISE equality in the
+exact dyadic regime, for integer work (index coverage, padding untouched) and for
+invariants (determinism, all configurations agree).
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def run_gpu(G, A, B, C0, alpha, beta, cfg=None):
+    dA, dB, dC = dev(A), dev(B), dev(C0)
+    G.gemm(dA, dB, dC, alpha, beta, cfg=cfg)
+    torch.cuda.synchronize()
+    return dC.cpu().numpy()
+
+
+def check_vs_oracle(C_gpu, A, B, C0, alpha, beta):
+    ref, mag = oracle.dgemm(alpha, A, B, beta, C0, want_mag=True)
+    r = oracle.check(C_gpu, ref, oracle.bound(A.shape[1], alpha, beta, mag, C0))
+    assert r.ok, str(r)
+    return r
+
+
+def all_cfgs(G):
+    return list(range(G.num_cfgs()))
+
+
+# ---------------------------------------------------------------- config 1
+@pytest.mark.parametrize("seed", [1706, 1, 2, 3])
+def test_config1_n256(cuda_lib, seed):
+    A, B, C0 = synth.problem(256, 256, 256, seed=seed)
+    C = run_gpu(cuda_lib, A, B, C0, 1.0, 0.0)
+    r = check_vs_oracle(C, A, B, C0, 1.0, 0.0)
+    assert r.max_ratio < 0.05   # a ratio near 1 would signal a bug even though it passes
+
+
+EDGE = [(1, 1, 1), (2, 2, 2), (7, 5, 3), (8, 16, 4), (31, 33, 17), (127, 129, 65), (129, 127, 257),
+        (257, 130, 33), (300, 333, 257), (65, 200, 1), (3, 1000, 40), (1000, 3, 40), (130, 130, 2000)]
+
+
+@pytest.mark.parametrize("shape", EDGE, ids=lambda s: "x".join(map(str, s)))
+def test_edge_shapes_every_cfg(cuda_lib, shape):
+    M, N, K = shape
+    A, B, C0 = synth.problem(M, N, K, seed=M * 7 + N)
+    tma_eligible = (K % 2 == 0) and (N % 2 == 0)   # packed lda = K, ldb = N: TMA needs 16-byte strides
+    ran = 0
+    for info in cuda_lib.cfgs():
+        if info["tma"] and not tma_eligible:
+            with pytest.raises(cuda_lib.GemmError) as ei:
+                run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=info["id"])
+            assert ei.value.code == cuda_lib.GEMM_ERR_UNSUPPORTED
+            continue
+        C = run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=info["id"])
+        check_vs_oracle(C, A, B, C0, 1.5, 0.5)
+        ran += 1
+    assert ran >= 2
+    # the heuristic path always works
+    check_vs_oracle(run_gpu(cuda_lib, A, B, C0, 1.5, 0.5), A, B, C0, 1.5, 0.5)
+
+
+@pytest.mark.parametrize("shape", [(0, 5, 5), (5, 0, 5)])
+def test_empty_is_noop(cuda_lib, shape):
+    M, N, K = shape
+    A, B, C0 = synth.problem(M, N, K)
+    C = run_gpu(cuda_lib, A, B, C0, 1.0, 0.0)
+    assert C.shape == (M, N)
+
+
+def test_k_zero_scales_C(cuda_lib):
+    C0 = synth.matrix("uniform", 1, 2, 70, 90)
+    dC = dev(C0)
+    dA = torch.empty((70, 0), dtype=torch.float64, device="cuda")
+    dB = torch.empty((0, 90), dtype=torch.float64, device="cuda")
+    cuda_lib.gemm(dA, dB, dC, 2.0, 0.25)
+    torch.cuda.synchronize()
+    assert np.array_equal(dC.cpu().numpy(), 0.25 * C0)
+
+
+def test_alpha_zero_does_not_read_AB(cuda_lib):
+    C0 = synth.matrix("uniform", 1, 2, 64, 48)
+    A = np.full((64, 32), np.nan)
+    B = np.full((32, 48), np.nan)
+    C = run_gpu(cuda_lib, A, B, C0, 0.0, 2.0)
+    assert np.array_equal(C, 2.0 * C0)
+
+
+def test_beta_zero_does_not_read_C(cuda_lib):
+    A, B, _ = synth.problem(200, 150, 64, seed=5)
+    C = run_gpu(cuda_lib, A, B, np.full((200, 150), np.nan), 1.0, 0.0)
+    assert np.all(np.isfinite(C))
+    check_vs_oracle(C, A, B, np.zeros((200, 150)), 1.0, 0.0)
+
+
+def test_nan_in_A_poisons_exactly_its_row(cuda_lib):
+    A, B, C0 = synth.problem(300, 260, 100, seed=6)
+    A[137, 42] = np.nan
+    C = run_gpu(cuda_lib, A, B, C0, 1.0, 0.0)
+    assert np.all(np.isnan(C[137]))
+    assert np.all(np.isfinite(np.delete(C, 137, axis=0)))
+
+
+# ---------------------------------------------------------------- exact regime
+@pytest.mark.parametrize("mode", ["dyadic", "int8"])
+def test_exact_regime_bitwise_every_cfg(cuda_lib, mode):
+    """Every partial sum is exact -> any summation order gives the same bits."""
+    A, B, C0 = synth.problem(520, 390, 1000, mode=mode, seed=2)
+    ref = oracle.dgemm(1.5, A, B, 0.5, C0)
+    for cfg in all_cfgs(cuda_lib):
+        C = run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=cfg)
+        assert np.array_equal(C, ref), cuda_lib.cfg_name(cfg)
+
+
+def test_all_cfgs_bitwise_identical_and_deterministic(cuda_lib):
+    """Every configuration sums each entry in the same order (16-deep k-groups ascending,
+    same k-permutation, same DMMA chain) -> identical bits; and runs repeat bitwise."""
+    A, B, C0 = synth.problem(334, 290, 778, seed=3)
+    outs = [run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=c) for c in all_cfgs(cuda_lib)]
+    for c, o in zip(all_cfgs(cuda_lib), outs):
+        assert np.array_equal(o, outs[0]), cuda_lib.cfg_name(c)
+    again = run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=0)
+    assert np.array_equal(again, outs[0])
+    check_vs_oracle(outs[0], A, B, C0, 1.5, 0.5)
+
+
+# ---------------------------------------------------------------- layout / padding
+def test_padded_leading_dimensions_untouched(cuda_lib):
+    """lda > K, ldb > N, ldc > N: padding holds NaN sentinels that must be neither read
+    nor written (bitwise unchanged)."""
+    M, N, K = 150, 140, 90
+    A, B, C0 = synth.problem(M, N, K, seed=8)
+    for pad in (2, 3, 5):   # even pads -> TMA path, odd -> generic path
+        Ap = np.full((M, K + pad), np.nan); Ap[:, :K] = A
+        Bp = np.full((K, N + pad), np.nan); Bp[:, :N] = B
+        Cp = np.full((M, N + pad), np.nan); Cp[:, :N] = C0
+        dA, dB, dC = dev(Ap), dev(Bp), dev(Cp)
+        cuda_lib.gemm(dA[:, :K], dB[:, :N], dC[:, :N], 1.5, 0.5)
+        torch.cuda.synchronize()
+        out = dC.cpu().numpy()
+        assert np.all(np.isnan(out[:, N:])), "padding columns of C were written"
+        check_vs_oracle(out[:, :N], A, B, C0, 1.5, 0.5)
+
+
+def test_misaligned_pointers_take_generic_path(cuda_lib):
+    M, N, K = 97, 101, 67
+    A, B, C0 = synth.problem(M, N, K, seed=9)
+    bufA = torch.zeros(M * K + 1, dtype=torch.float64, device="cuda")
+    bufB = torch.zeros(K * N + 1, dtype=torch.float64, device="cuda")
+    bufC = torch.zeros(M * N + 1, dtype=torch.float64, device="cuda")
+    dA = bufA[1:].view(M, K); dA.copy_(dev(A))
+    dB = bufB[1:].view(K, N); dB.copy_(dev(B))
+    dC = bufC[1:].view(M, N); dC.copy_(dev(C0))
+    cuda_lib.gemm(dA, dB, dC, 1.0, 1.0)
+    torch.cuda.synchronize()
+    check_vs_oracle(dC.cpu().numpy(), A, B, C0, 1.0, 1.0)
+    tma_ids = [c["id"] for c in cuda_lib.cfgs() if c["tma"]]
+    with pytest.raises(cuda_lib.GemmError) as ei:
+        cuda_lib.gemm(dA, dB, dC, 1.0, 1.0, cfg=tma_ids[0])
+    assert ei.value.code == cuda_lib.GEMM_ERR_UNSUPPORTED
+
+
+def test_argument_errors_enqueue_nothing(cuda_lib):
+    G = cuda_lib
+    C = torch.full((8, 8), 7.0, dtype=torch.float64, device="cuda")
+    A = torch.ones((8, 8), dtype=torch.float64, device="cuda")
+    rc = G.gemm_raw(8, 8, 8, 1.0, A.data_ptr(), 4, A.data_ptr(), 8, 0.0, C.data_ptr(), 8)
+    assert rc == G.GEMM_ERR_ARG and "lda" in G.last_error()
+    rc = G.gemm_raw(8, 8, 8, 1.0, A.data_ptr(), 8, A.data_ptr(), 8, 0.0, A.data_ptr(), 8)
+    assert rc == G.GEMM_ERR_ARG and "overlap" in G.last_error()
+    rc = G.gemm_raw(-1, 8, 8, 1.0, A.data_ptr(), 8, A.data_ptr(), 8, 0.0, C.data_ptr(), 8)
+    assert rc == G.GEMM_ERR_ARG and "M=" in G.last_error()
+    rc = G.gemm_raw(8, 8, 8, 1.0, A.data_ptr(), 8, A.data_ptr(), 8, 0.0, C.data_ptr(), 8, cfg=10 ** 6)
+    assert rc == G.GEMM_ERR_ARG and "cfg_id" in G.last_error()
+    torch.cuda.synchronize()
+    assert torch.all(C == 7.0)
+
+
+# ---------------------------------------------------------------- inputs
+@pytest.mark.parametrize("mode", list(synth.MODES))
+def test_device_generator_matches_synth_bitwise(cuda_lib, mode):
+    rows, cols = 301, 129
+    X = torch.empty((rows, cols), dtype=torch.float64, device="cuda")
+    cuda_lib.fill(X, mode, 1706, 1)
+    torch.cuda.synchronize()
+    assert np.array_equal(X.cpu().numpy(), synth.matrix(mode, 1706, 1, rows, cols))
+    slab = torch.empty((50, cols), dtype=torch.float64, device="cuda")
+    cuda_lib.fill(slab, mode, 1706, 1, rows=rows, row0=100)
+    torch.cuda.synchronize()
+    assert np.array_equal(slab.cpu().numpy(), synth.matrix(mode, 1706, 1, rows, cols, row0=100, nrows=50))
+
+
+# ---------------------------------------------------------------- sizes of config 2 / 3
+def _sampled_rows_check(G, M, N, K, alpha, beta, rows, mode="uniform", seed=1706):
+    dA = torch.empty((M, K), dtype=torch.float64, device="cuda")
+    dB = torch.empty((K, N), dtype=torch.float64, device="cuda")
+    dC = torch.empty((M, N), dtype=torch.float64, device="cuda")
+    G.fill(dA, mode, seed, synth.MAT_A)
+    G.fill(dB, mode, seed, synth.MAT_B)
+    G.fill(dC, mode, seed, synth.MAT_C)
+    G.gemm(dA, dB, dC, alpha, beta)
+    torch.cuda.synchronize()
+    B = synth.matrix(mode, seed, synth.MAT_B, K, N)
+    A_r = np.vstack([synth.matrix(mode, seed, synth.MAT_A, M, K, row0=r, nrows=1) for r in rows])
+    C0_r = np.vstack([synth.matrix(mode, seed, synth.MAT_C, M, N, row0=r, nrows=1) for r in rows])
+    ref, mag = oracle.dgemm(alpha, A_r, B, beta, C0_r, want_mag=True)
+    got = dC[torch.tensor(rows, device="cuda")].cpu().numpy()
+    res = oracle.check(got, ref, oracle.bound(K, alpha, beta, mag, C0_r))
+    assert res.ok, f"rows {rows}: {res}"
+    del dA, dB, dC
+    torch.cuda.empty_cache()
+    return res.max_ratio
+
+
+def _rows(M, bm=128, extra=8, seed=0):
+    rng = np.random.default_rng(seed)
+    s = {0, M - 1, bm - 1, bm, M // 2, M - bm} | set(int(x) for x in rng.integers(0, M, extra))
+    return sorted(r for r in s if 0 <= r < M)
+
+
+@pytest.mark.parametrize("n", [1024, 2048])
+def test_config2_full_oracle(cuda_lib, n):
+    A, B, C0 = synth.problem(n, n, n, seed=1706)
+    C = run_gpu(cuda_lib, A, B, C0, 1.0, 0.0)
+    check_vs_oracle(C, A, B, C0, 1.0, 0.0)
+
+
+def test_config3_n8192_alpha_beta_sampled_rows(cuda_lib):
+    _sampled_rows_check(cuda_lib, 8192, 8192, 8192, 1.5, 0.5, _rows(8192, extra=6))
+
+
+def test_config2_n16384_sampled_rows_bench_launch(cuda_lib):
+    """The bench workload (16384^3, alpha=1, beta=0, heuristic config = bench launch)."""
+    _sampled_rows_check(cuda_lib, 16384, 16384, 16384, 1.0, 0.0, _rows(16384, extra=4))
+
+
+def test_n16384_dyadic_sampled_rows_bitwise(cuda_lib):
+    M = N = K = 16384
+    dA = torch.empty((M, K), dtype=torch.float64, device="cuda")
+    dB = torch.empty((K, N), dtype=torch.float64, device="cuda")
+    dC = torch.empty((M, N), dtype=torch.float64, device="cuda")
+    for X, m in ((dA, 0), (dB, 1), (dC, 2)):
+        cuda_lib.fill(X, "dyadic", 7, m)
+    cuda_lib.gemm(dA, dB, dC, 1.5, 0.5)
+    torch.cuda.synchronize()
+    B = synth.matrix("dyadic", 7, 1, K, N)
+    rows = _rows(M, extra=2)
+    A_r = np.vstack([synth.matrix("dyadic", 7, 0, M, K, row0=r, nrows=1) for r in rows])
+    C0_r = np.vstack([synth.matrix("dyadic", 7, 2, M, N, row0=r, nrows=1) for r in rows])
+    ref = oracle.dgemm(1.5, A_r, B, 0.5, C0_r)
+    assert np.array_equal(dC[torch.tensor(rows, device="cuda")].cpu().numpy(), ref)
+    del dA, dB, dC
+    torch.cuda.empty_cache()
+
+
+# ---------------------------------------------------------------- host entry point (e2e)
+def test_host_entry_point(cuda_lib):
+    A, B, C0 = synth.problem(700, 650, 300, seed=4)
+    C = C0.copy()
+    cuda_lib.gemm_host(A, B, C, 1.5, 0.5)
+    check_vs_oracle(C, A, B, C0, 1.5, 0.5)
+    # same bits as the device entry point (row panels do not change per-entry arithmetic)
+    assert np.array_equal(C, run_gpu(cuda_lib, A, B, C0, 1.5, 0.5))
+
+
+def test_host_entry_point_large_pinned(cuda_lib):
+    M, N, K = 5000, 3000, 1000
+    A, B, C0 = synth.problem(M, N, K, seed=11)
+    tA = torch.from_numpy(A).pin_memory()
+    tB = torch.from_numpy(B).pin_memory()
+    tC = torch.from_numpy(C0.copy()).pin_memory()
+    cuda_lib.gemm_host(tA, tB, tC, 1.0, 1.0)
+    assert np.array_equal(tC.numpy(), run_gpu(cuda_lib, A, B, C0, 1.0, 1.0))
+    rows = _rows(M, extra=4)
+    ref, mag = oracle.dgemm(1.0, A[rows], B, 1.0, C0[rows], want_mag=True)
+    r = oracle.check(tC.numpy()[rows], ref, oracle.bound(K, 1.0, 1.0, mag, C0[rows]))
+    assert r.ok, str(r)
+
+
+# ---------------------------------------------------------------- sharded (1 GPU, NCCL world=1)
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_sharded_world1_equals_single_gpu(cuda_lib, chunks):
+    M, N, K = 400, 520, 300
+    A, B, C0 = synth.problem(M, N, K, seed=12)
+    comm = cuda_lib.Comm(0, 1)
+    dA, dB, dC = dev(A), dev(B), dev(C0)
+    comm.gemm_sharded(dA, dB, dC, 1.5, 0.5, root=0, bcast_chunks=chunks)
+    torch.cuda.synchronize()
+    comm.close()
+    assert np.array_equal(dC.cpu().numpy(), run_gpu(cuda_lib, A, B, C0, 1.5, 0.5))
+
+
+def test_fake_multi_gpu_row_partition(cuda_lib):
+    """The P-rank row partition run sequentially on one GPU equals the full GEMM bitwise
+    (isolates partition/offset bugs from communication)."""
+    M, N, K = 1001, 300, 257
+    A, B, C0 = synth.problem(M, N, K, seed=13)
+    full = run_gpu(cuda_lib, A, B, C0, 1.0, 1.0)
+    for P in (2, 3, 8):
+        out = np.empty_like(full)
+        for r in range(P):
+            r0, r1 = cuda_lib.row_range(M, r, P)
+            out[r0:r1] = run_gpu(cuda_lib, A[r0:r1], B, C0[r0:r1], 1.0, 1.0)
+        assert np.array_equal(out, full), P
+
+
+# ---------------------------------------------------------------- microbenchmark
+def test_peak_probe_runs(cuda_lib):
+    out = torch.zeros(148, dtype=torch.float64, device="cuda")
+    cyc = torch.zeros(1, dtype=torch.int64, device="cuda")
+    cuda_lib.peak_probe("dmma", 148, 8, 1000, out, cyc)
+    cuda_lib.peak_probe("dfma", 148, 8, 1000, out, cyc)
+    torch.cuda.synchronize()
+    assert int(cyc.item()) > 0
