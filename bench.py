@@ -266,10 +266,7 @@ def main():
     t_ms = e_start.elapsed_time(e_end)
     k_ms = [s.elapsed_time(e) for s, e in kev]
     k_mean = statistics.mean(k_ms)
-    if world > 1:
-        t = torch.tensor([t_ms, k_mean], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_ms, k_mean = float(t[0]), float(t[1])
+    t_ms, k_mean = G.max_over_ranks([t_ms, k_mean], world, device="cuda")
     flops_step = 2.0 * M * N * K
     value = flops_step * a.steps / (t_ms * 1e-3) / 1e12
     flops_local = 2.0 * Ml * N * K
@@ -325,10 +322,7 @@ def main():
             G.gemm_host(hA, hB, hC, 1.0, 0.0)
             ts.append(time.perf_counter() - t0)
         e2e_s = sum(ts)
-        if world > 1:
-            t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_s = float(t[0])
+        e2e_s = G.max_over_ranks([e2e_s], world, device="cuda")[0]
         G.host_pool_release()
         e2e = {"value": flops_step * a.e2e_steps / e2e_s / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": 8 * (M * K + world * K * N), "d2h_bytes_per_step": 8 * M * N,

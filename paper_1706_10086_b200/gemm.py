@@ -227,19 +227,10 @@ class Comm:
     created on rank 0 and distributed with torch.distributed (any backend)."""
 
     def __init__(self, rank: int, world: int, group=None):
-        import torch
-        import torch.distributed as dist
-        idbuf = ctypes.create_string_buffer(128)
-        if rank == 0:
-            _check(_lib.gemm_comm_unique_id(idbuf))
-        payload = [bytes(idbuf.raw)] if rank == 0 else [None]
-        if world > 1:
-            dist.broadcast_object_list(payload, src=0, group=group)
-        raw = payload[0]
+        raw = share_unique_id(rank, world, group)
         self._h = ctypes.c_void_p()
         _check(_lib.gemm_comm_init(ctypes.byref(self._h), world, ctypes.create_string_buffer(raw, 128), rank))
         self.rank, self.world = rank, world
-        self._torch = torch
 
     @property
     def handle(self):
@@ -268,6 +259,37 @@ class Comm:
             self.close()
         except Exception:
             pass
+
+
+def unique_id() -> bytes:
+    """A fresh 128-byte NCCL unique id (gemm_comm_unique_id)."""
+    idbuf = ctypes.create_string_buffer(128)
+    _check(_lib.gemm_comm_unique_id(idbuf))
+    return bytes(idbuf.raw)
+
+
+def share_unique_id(rank: int, world: int, group=None) -> bytes:
+    """Rank 0 creates the id; every rank returns the same 128 bytes (torch.distributed,
+    any backend -- gloo in the CPU tests, nccl in bench.py)."""
+    payload = [unique_id() if rank == 0 else None]
+    if world > 1:
+        import torch.distributed as dist
+        dist.broadcast_object_list(payload, src=0, group=group)
+    raw = payload[0]
+    if not isinstance(raw, (bytes, bytearray)) or len(raw) != 128:
+        raise RuntimeError("NCCL unique id distribution failed")
+    return bytes(raw)
+
+
+def max_over_ranks(values, world: int, device=None):
+    """Element-wise max over ranks of a list of floats (timing is max over ranks)."""
+    if world <= 1:
+        return [float(v) for v in values]
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(v) for v in values], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t.cpu()]
 
 
 def row_range(M: int, rank: int, world: int) -> tuple:

@@ -1,0 +1,181 @@
+"""CPU-side checks of the C-ABI library (no GPU needed, no compute calls).
+
+* the library builds for sm_100a and loads;
+* it exports every symbol include/gemm_f64.h declares, and the binding knows them;
+* the SASS of every GEMM kernel uses the FP64 tensor pipe (DMMA.8x8x4), TMA
+  kernels issue UTMALDG, no kernel spills to local memory, and the epilogue has
+  256-bit stores (the Listing-2 "disassembly inspection" analog);
+* argument validation (runs before any CUDA call) rejects bad arguments with a
+  message naming them, and the configuration registry is consistent.
+"""
+
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "gemm_f64.h")
+
+
+@pytest.fixture(scope="module")
+def G():
+    from paper_1706_10086_b200 import build
+    build.build()
+    from paper_1706_10086_b200 import gemm
+    return gemm
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"GEMM_API\s+(?:const\s+)?\w+\s*\*?\s*(gemm_\w+)\s*\(", src)))
+
+
+def test_header_declares_and_library_exports_every_symbol(G):
+    decl = declared_symbols()
+    assert len(decl) >= 15
+    out = subprocess.run(["nm", "-D", "--defined-only", G.LIB_PATH], capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r"\sT\s(gemm_\w+)$", out, flags=re.M))
+    missing = [s for s in decl if s not in exported]
+    assert not missing, missing
+    assert set(decl) == set(G.EXPORTS)
+    # nothing but the C ABI is exported (internal C++ symbols are hidden)
+    assert all(s.startswith("gemm_") for s in exported)
+
+
+def test_library_is_sm100a_only(G):
+    out = subprocess.run(["cuobjdump", "--list-elf", G.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out), out
+
+
+@pytest.fixture(scope="module")
+def sass(G):
+    return subprocess.run(["cuobjdump", "-sass", G.LIB_PATH], capture_output=True, text=True, check=True).stdout
+
+
+def _functions(sass):
+    funcs = {}
+    cur = None
+    for line in sass.splitlines():
+        m = re.match(r"\s+Function : (\S+)", line)
+        if m:
+            cur = m.group(1)
+            funcs[cur] = []
+        elif cur:
+            funcs[cur].append(line)
+    return {k: "\n".join(v) for k, v in funcs.items()}
+
+
+def test_sass_gemm_kernels_use_dmma_tma_and_no_spills(sass):
+    funcs = _functions(sass)
+    gemm = {k: v for k, v in funcs.items() if "dgemm_" in k}
+    assert gemm, "no GEMM kernels found"
+    for name, body in gemm.items():
+        assert "DMMA.8x8x4" in body, name
+        assert not re.search(r"\b(LDL|STL)\b", body), f"local-memory spill in {name}"
+        if "dgemm_tma_kernel" in name:
+            assert "UTMALDG" in body, name
+            assert "STG.E.ENL2.256" in body, name
+        if "dgemm_generic_kernel" in name:
+            assert "LDGSTS" in body, name
+
+
+def test_ptxas_reports_no_spills(G):
+    from paper_1706_10086_b200 import build
+    for f in os.listdir(build.BUILD):
+        if f.endswith(".ptxas.txt"):
+            txt = open(os.path.join(build.BUILD, f)).read()
+            for m in re.finditer(r"(\d+) bytes spill stores, (\d+) bytes spill loads", txt):
+                assert m.group(1) == "0" and m.group(2) == "0", f
+
+
+def test_cfg_registry(G):
+    n = G.num_cfgs()
+    assert n >= 5
+    names = set()
+    for info in G.cfgs():
+        names.add(info["name"])
+        assert info["bm"] % info["wm"] == 0 and info["bn"] % info["wn"] == 0
+        assert info["threads"] == 32 * (info["bm"] // info["wm"]) * (info["bn"] // info["wn"])
+        assert info["smem_bytes"] <= 227 * 1024
+        stage = 8 * (info["bm"] + info["bn"]) * info["bk"]      # Eq. (5) analog: 2 tiles per stage
+        assert info["smem_bytes"] >= info["stages"] * stage
+        assert info["e"] == info["wm"] * info["wn"] // 32
+        assert re.match(r"(tma|gen)_\d+x\d+x\d+_w\d+x\d+_s\d+", info["name"])
+    assert len(names) == n
+    # the paper's P100 optimum (16x16 threads x T=4 -> 64x64 block tile, E=16) is a grid point
+    assert any(i["bm"] == 64 and i["bn"] == 64 and i["e"] == 16 for i in G.cfgs())
+    with pytest.raises(G.GemmError):
+        G.cfg_name(n)
+
+
+def test_heuristic_selection(G):
+    big = G.cfg_info(G.cfg_select(16384, 16384, 16384, 0, 16384, 0, 16384))
+    assert big["tma"] == 1 and big["bm"] * big["bn"] >= 128 * 128
+    odd = G.cfg_info(G.cfg_select(1000, 1000, 1001, 0, 1001, 0, 1000))
+    assert odd["tma"] == 0       # odd lda -> not TMA-eligible
+    mis = G.cfg_info(G.cfg_select(4096, 4096, 4096, 8, 4096, 0, 4096))
+    assert mis["tma"] == 0       # 8-byte (not 16-byte) aligned A
+
+
+@pytest.mark.parametrize("args,needle", [
+    ((-1, 4, 4, 1.0, 16, 4, 16, 4, 0.0, 16, 4), "M=-1"),
+    ((4, -1, 4, 1.0, 16, 4, 16, 4, 0.0, 16, 4), "N=-1"),
+    ((4, 4, -2, 1.0, 16, 4, 16, 4, 0.0, 16, 4), "K=-2"),
+    ((4, 4, 8, 1.0, 16, 4, 16, 4, 0.0, 16, 4), "lda=4"),
+    ((4, 8, 4, 1.0, 16, 4, 16, 4, 0.0, 16, 8), "ldb=4"),
+    ((4, 8, 4, 1.0, 16, 4, 16, 8, 0.0, 16, 4), "ldc=4"),
+    ((4, 4, 4, 1.0, 16, 4, 16, 4, 0.0, None, 4), "C is NULL"),
+    ((4, 4, 4, 1.0, None, 4, 16, 4, 0.0, 4096, 4), "A is NULL"),
+    ((4, 4, 4, 1.0, 16, 4, None, 4, 0.0, 4096, 4), "B is NULL"),
+    ((4, 4, 4, 1.0, 12, 4, 16, 4, 0.0, 4096, 4), "A is not 8-byte aligned"),
+    ((4, 4, 4, 1.0, 1024, 4, 4096, 4, 0.0, 1040, 4), "C overlaps A"),
+    ((4, 4, 4, 1.0, 1024, 4, 4096, 4, 0.0, 4100 - 4, 4), "C overlaps B"),
+    ((2 ** 31, 4, 4, 1.0, 16, 4, 16, 4, 0.0, 16, 4), "< 2^31"),
+])
+def test_argument_validation_messages(G, args, needle):
+    rc = G.gemm_raw(*args)
+    assert rc in (G.GEMM_ERR_ARG, G.GEMM_ERR_UNSUPPORTED)
+    assert needle in G.last_error(), G.last_error()
+
+
+def test_bad_cfg_id_rejected(G):
+    rc = G.gemm_raw(4, 4, 4, 1.0, 16, 4, 16, 4, 0.0, 4096, 4, cfg=999)
+    assert rc == G.GEMM_ERR_ARG and "cfg_id" in G.last_error()
+
+
+def test_sharded_argument_validation(G):
+    import ctypes
+    lib = G.lib()
+    rc = lib.gemm_f64_sharded(4, 4, 4, 1.0, 16, 4, 16, 4, 0.0, 4096, 4, None, 0, 1, None)
+    assert rc == G.GEMM_ERR_ARG and "comm" in G.last_error()
+    h = ctypes.c_void_p()
+    rc = lib.gemm_comm_init(ctypes.byref(h), 2, ctypes.create_string_buffer(128), 5)
+    assert rc == G.GEMM_ERR_ARG and "rank" in G.last_error()
+
+
+def test_fill_and_probe_validation(G):
+    lib = G.lib()
+    assert lib.gemm_fill_f64(9, 1, 0, 4, 4, 0, 4, 16, 4, None) == G.GEMM_ERR_ARG
+    assert lib.gemm_fill_f64(0, 1, 0, 4, 4, 2, 4, 16, 4, None) == G.GEMM_ERR_ARG   # slab outside
+    assert lib.gemm_peak_probe(3, 1, 1, 1, 16, None, None) == G.GEMM_ERR_ARG
+
+
+def test_row_range_partition(G):
+    for M in (0, 1, 7, 16384, 32768, 65537):
+        for P in (1, 2, 3, 4, 8):
+            parts = [G.row_range(M, r, P) for r in range(P)]
+            assert parts[0][0] == 0 and parts[-1][1] == M
+            for (a0, a1), (b0, b1) in zip(parts, parts[1:]):
+                assert a1 == b0 and a0 <= a1
+            sizes = [b - a for a, b in parts]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        G.row_range(10, 2, 2)
+
+
+def test_unique_id_is_128_bytes_and_fresh(G):
+    a, b = G.unique_id(), G.unique_id()
+    assert len(a) == 128 and len(b) == 128 and a != b
