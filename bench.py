@@ -283,9 +283,9 @@ def main():
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         pj = json.load(open(prof))
-        key = f"{Ml}x{N}x{K}"
-        if key in pj:
-            traffic = pj[key]["dram_bytes_per_launch"]
+        ent = pj.get(f"{Ml}x{N}x{K}")
+        if ent and ent.get("kernel") == cfg_name:   # only a capture of this very kernel counts
+            traffic = ent["dram_bytes_per_launch"]
     except (OSError, ValueError, KeyError):
         pass
     roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_DATASHEET_TFLOPS, "unit": "TFLOP/s",

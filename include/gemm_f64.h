@@ -91,6 +91,14 @@ GEMM_API int gemm_f64_cfg(int64_t M, int64_t N, int64_t K, double alpha,
                  const double *A, int64_t lda, const double *B, int64_t ldb,
                  double beta, double *C, int64_t ldc, int cfg_id, void *cuda_stream);
 
+/* Same as gemm_f64_cfg, additionally forcing the number of deterministic split-K
+ * slices for a *_splitk configuration (splits = 0: the model's choice; 1: no
+ * split).  Forcing splits > 1 on a configuration without split-K returns
+ * GEMM_ERR_UNSUPPORTED. */
+GEMM_API int gemm_f64_ex(int64_t M, int64_t N, int64_t K, double alpha,
+                const double *A, int64_t lda, const double *B, int64_t ldb,
+                double beta, double *C, int64_t ldc, int cfg_id, int splits, void *cuda_stream);
+
 /* Host-buffer entry point ("the call a user makes" with host data): A, B, C are
  * HOST pointers (pinned for full copy/compute overlap; pageable works but
  * serialises).  The library allocates device buffers from a cached pool, copies
@@ -113,7 +121,7 @@ typedef struct {
     int threads;        /* threads per CTA (lane 0 of warp 0 doubles as TMA producer) */
     int smem_bytes;     /* dynamic shared memory per CTA                           */
     int tma;            /* 1: TMA + mbarrier pipeline; 0: cp.async staging          */
-    int split_k;        /* >1: deterministic split-K kernel family                */
+    int split_k;        /* 1: no split-K; 0: deterministic split-K, slices chosen per call */
     int regs;           /* registers per thread (from cudaFuncGetAttributes; 0 before first use) */
 } gemm_cfg_desc;
 
@@ -124,6 +132,13 @@ GEMM_API int gemm_cfg_info(int cfg_id, gemm_cfg_desc *out);
 /* The configuration the heuristic picks for this shape / alignment. */
 GEMM_API int gemm_cfg_select(int64_t M, int64_t N, int64_t K, const double *A, int64_t lda,
                     const double *B, int64_t ldb);
+
+/* The full launch plan of the heuristic: configuration id and number of
+ * deterministic split-K slices (1 = no split; >1 only for *_splitk configurations:
+ * each slice multiplies a contiguous k-range into a workspace partial and the
+ * last slice to finish sums the partials in slice order, row a5). */
+GEMM_API int gemm_plan(int64_t M, int64_t N, int64_t K, const double *A, int64_t lda,
+              const double *B, int64_t ldb, int *cfg_id, int *splits);
 
 /* Thread-local message for the last non-OK return on this thread. */
 GEMM_API const char *gemm_last_error(void);

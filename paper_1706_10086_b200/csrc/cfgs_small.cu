@@ -1,0 +1,29 @@
+// cfgs_small.cu -- TMA configurations with 128x64 / 64x128 / 64x64 CTA tiles (mid-size and small problems;
+// 64x64 with E=16 is the paper's P100 optimum, 16x16 threads x T=4, Tab. 4).
+#include "registry.cuh"
+
+namespace dg {
+
+static const CfgEntry k_table[] = {
+    DG_TMA(128, 64, 16, 64, 32, 4),
+    DG_TMA(128, 64, 16, 32, 32, 6),
+    DG_TMA(128, 64, 16, 32, 16, 6),
+    DG_TMA(64, 128, 16, 32, 64, 4),
+    DG_TMA(64, 128, 16, 32, 32, 6),
+    DG_TMA(64, 128, 16, 16, 32, 6),
+    DG_TMA(64, 64, 16, 64, 32, 6),
+    DG_TMA(64, 64, 16, 32, 32, 6),
+    DG_TMA(64, 64, 16, 32, 16, 6),
+    DG_TMA(64, 64, 16, 16, 32, 6),
+    DG_TMA_SPLIT(64, 64, 16, 32, 16, 6),
+    DG_TMA_SPLIT(128, 64, 16, 32, 16, 6),
+    DG_TMA_SPLIT(64, 128, 16, 32, 64, 4),
+    DG_TMA_SPLIT(128, 128, 16, 32, 32, 4),
+};
+
+const CfgEntry *cfg_table_small(int *n) {
+    *n = (int)(sizeof(k_table) / sizeof(k_table[0]));
+    return k_table;
+}
+
+}  // namespace dg

@@ -57,6 +57,8 @@ struct Cfg {
     static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr uint32_t BAR_BYTES = 2 * STAGES * 8;
     static constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + BAR_BYTES + 1024;  // +1024: manual alignment
+    // two CTAs per SM when shared memory allows it (227 KB per SM usable, ~1 KB reserved per CTA)
+    static constexpr int MIN_BLOCKS = (2 * (SMEM_BYTES + 1024) <= 228 * 1024) ? 2 : 1;
 };
 
 // k-permutation inside a 16-deep k-group.  A thread with MMA k-index t (= lane & 3)
@@ -201,11 +203,72 @@ __device__ __forceinline__ void tma_issue_stage(uint8_t *stage_ptr, const CUtens
     }
 }
 
+// Deterministic split-K (row a5, small shapes): gridDim.y = splits; split s of a tile
+// multiplies k-steps [s*KT/S, (s+1)*KT/S) into a raw (unscaled) partial.  Every split
+// stores its partial to the workspace; the CTA that arrives last on the tile's counter
+// sums the S partials in the fixed order s = 0, 1, ..., S-1 and runs the epilogue, so
+// the result does not depend on which CTA finishes last.  The counter is reset by that
+// CTA, leaving the workspace ready for the next launch on the same stream.
+struct SplitArgs {
+    int splits;        // 1 = no split
+    double *ws;        // [tiles][splits][E/4][warps][32][4] doubles
+    int *counters;     // [tiles], zero between launches
+};
+
 template <class C>
-__global__ void __launch_bounds__(C::CONSUMER_THREADS, 1)
+__device__ __forceinline__ double *split_slot(const SplitArgs &sk, int tile, int s, int warp, int lane) {
+    constexpr int Q = C::E / 4;   // 256-bit groups per thread
+    return sk.ws + (((int64_t)tile * sk.splits + s) * Q * C::CONSUMER_WARPS * 32 + (int64_t)warp * 32 + lane) * 4;
+}
+
+// returns true if this CTA must run the epilogue (no split, or last split to arrive)
+template <class C>
+__device__ __forceinline__ bool split_reduce(double (&acc)[C::MB][C::NP][2][2], const SplitArgs &sk, int tile,
+                                             int s, int warp, int lane) {
+    if (sk.splits <= 1) return true;
+    constexpr int Q = C::E / 4;
+    constexpr int64_t QSTRIDE = (int64_t)C::CONSUMER_WARPS * 32 * 4;   // doubles between q groups
+    double *mine = split_slot<C>(sk, tile, s, warp, lane);
+    double *flat = &acc[0][0][0][0];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) stg_v4(mine + q * QSTRIDE, flat[4 * q], flat[4 * q + 1], flat[4 * q + 2], flat[4 * q + 3]);
+    __threadfence();
+    __syncthreads();
+    __shared__ int s_last;
+    if (threadIdx.x == 0) {
+        const int old = atomicAdd(&sk.counters[tile], 1);
+        s_last = (old == sk.splits - 1);
+    }
+    __syncthreads();
+    if (!s_last) return false;
+    __threadfence();
+#pragma unroll
+    for (int e = 0; e < C::E; ++e) flat[e] = 0.0;
+    for (int t = 0; t < sk.splits; ++t) {
+        const double *src = split_slot<C>(sk, tile, t, warp, lane);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            double v0, v1, v2, v3;
+            asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];\n"
+                         : "=d"(v0), "=d"(v1), "=d"(v2), "=d"(v3)
+                         : "l"(src + q * QSTRIDE));
+            flat[4 * q] += v0;
+            flat[4 * q + 1] += v1;
+            flat[4 * q + 2] += v2;
+            flat[4 * q + 3] += v3;
+        }
+    }
+    if (threadIdx.x == 0) sk.counters[tile] = 0;
+    return true;
+}
+
+// SPLIT = false instantiations carry no split-K code (the reduction's registers would
+// otherwise raise the 256x64/64x32 kernel from 199 to 255 registers).
+template <class C, bool SPLIT>
+__global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
     dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
                      int N, int K, double alpha, double beta, double *__restrict__ Cm, int64_t ldc, int vec,
-                     int group_m) {
+                     int group_m, SplitArgs sk) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
@@ -219,6 +282,10 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, 1)
     const int m0 = tm * C::BM, n0 = tn * C::BN;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int KT = (K + C::BK - 1) / C::BK;
+    const int split = SPLIT ? (int)blockIdx.y : 0;
+    const int nsplit = SPLIT ? sk.splits : 1;
+    const int kt0 = (int)(((int64_t)split * KT) / nsplit);
+    const int NK = (int)(((int64_t)(split + 1) * KT) / nsplit) - kt0;   // k-steps of this CTA
     const bool producer = (threadIdx.x == 0);
     uint64_t pol = 0;
 
@@ -232,8 +299,8 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, 1)
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
         pol = l2_policy_evict_normal();
-        for (int s = 0; s < C::STAGES && s < KT; ++s)
-            tma_issue_stage<C>(base_ptr + s * C::STAGE_BYTES, &tmA, &tmB, &full[s], m0, n0, s, pol);
+        for (int s = 0; s < C::STAGES && s < NK; ++s)
+            tma_issue_stage<C>(base_ptr + s * C::STAGE_BYTES, &tmA, &tmB, &full[s], m0, n0, kt0 + s, pol);
     }
     __syncthreads();
 
@@ -247,21 +314,24 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, 1)
 #pragma unroll
             for (int j = 0; j < 2; ++j) acc[mb][np][j][0] = acc[mb][np][j][1] = 0.0;
 
-    for (int kt = 0; kt < KT; ++kt) {
-        const int s = kt % C::STAGES;
-        if (producer && kt > 0) {
-            const int kn = kt - 1 + C::STAGES;   // refill the slot released at kt-1
-            if (kn < KT) {
-                const int sp = (kt - 1) % C::STAGES;
-                mbar_wait(&empty[sp], ((kt - 1) / C::STAGES) & 1);
-                tma_issue_stage<C>(base_ptr + sp * C::STAGE_BYTES, &tmA, &tmB, &full[sp], m0, n0, kn, pol);
+    for (int i = 0; i < NK; ++i) {
+        const int s = i % C::STAGES;
+        if (producer && i > 0) {
+            const int in = i - 1 + C::STAGES;   // refill the slot released at i-1
+            if (in < NK) {
+                const int sp = (i - 1) % C::STAGES;
+                mbar_wait(&empty[sp], ((i - 1) / C::STAGES) & 1);
+                tma_issue_stage<C>(base_ptr + sp * C::STAGE_BYTES, &tmA, &tmB, &full[sp], m0, n0, kt0 + in, pol);
             }
         }
-        mbar_wait(&full[s], (kt / C::STAGES) & 1);
+        mbar_wait(&full[s], (i / C::STAGES) & 1);
         const uint32_t sA = base + s * C::STAGE_BYTES;
         mma_stage<C>(sA, sA + C::A_BYTES, fo, acc);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    if constexpr (SPLIT) {
+        if (!split_reduce<C>(acc, sk, blockIdx.x, split, warp, lane)) return;
     }
     epilogue<C>(acc, m0 + warp_m * C::WM, n0 + warp_n * C::WN, lane, M, N, alpha, beta, Cm, ldc, vec != 0);
 }
@@ -344,17 +414,6 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, 1)
     }
     cp_async_wait<0>();
     epilogue<C>(acc, m0 + warp_m * C::WM, n0 + warp_n * C::WN, lane, M, N, alpha, beta, Cm, ldc, vec != 0);
-}
-
-// C = beta*C (alpha == 0 or K == 0); beta == 0 writes zeros without reading C.
-__global__ void scale_kernel(int M, int N, double beta, double *__restrict__ Cm, int64_t ldc) {
-    const int64_t total = (int64_t)M * N;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = idx / N, j = idx % N;
-        double *p = Cm + i * ldc + j;
-        *p = (beta == 0.0) ? 0.0 : beta * *p;
-    }
 }
 
 }  // namespace dg

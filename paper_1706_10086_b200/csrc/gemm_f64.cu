@@ -12,16 +12,32 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <set>
 #include <string>
+#include <tuple>
 #include <utility>
+#include <vector>
 
 #include "../../include/gemm_f64.h"
 #include "dgemm_kernels.cuh"
 #include "internal.h"
+#include "registry.cuh"
 
 namespace dg {
+
+// C = beta*C (alpha == 0 or K == 0); beta == 0 writes zeros without reading C.
+__global__ void scale_kernel(int M, int N, double beta, double *__restrict__ Cm, int64_t ldc) {
+    const int64_t total = (int64_t)M * N;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = idx / N, j = idx % N;
+        double *p = Cm + i * ldc + j;
+        *p = (beta == 0.0) ? 0.0 : beta * *p;
+    }
+}
+
 
 // ------------------------------------------------------------------ errors
 static thread_local std::string g_last_error;
@@ -58,7 +74,49 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // Row-major rows x cols matrix with leading dimension ld; box = box_rows x 16 doubles (128 B).
-static int make_tmap(CUtensorMap *map, const double *ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+// Encoded maps are cached (direct-mapped, keyed by every encode argument): a host-side
+// encode costs about a microsecond, which matters for small, launch-bound GEMMs.
+struct TmapKey {
+    const double *ptr;
+    int64_t rows, cols, ld;
+    int box_rows;
+    bool operator==(const TmapKey &o) const {
+        return ptr == o.ptr && rows == o.rows && cols == o.cols && ld == o.ld && box_rows == o.box_rows;
+    }
+};
+struct TmapSlot {
+    bool valid = false;
+    TmapKey key{};
+    CUtensorMap map;
+};
+static constexpr int kTmapSlots = 256;
+static TmapSlot g_tmap_cache[kTmapSlots];
+static std::mutex g_tmap_mu;
+
+static int encode_tmap(CUtensorMap *map, const double *ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows);
+
+int make_tmap(CUtensorMap *map, const double *ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+    const TmapKey key{ptr, rows, cols, ld, box_rows};
+    const uint64_t h = ((uint64_t)(uintptr_t)ptr * 0x9E3779B97F4A7C15ull) ^ ((uint64_t)rows * 0xC2B2AE3D27D4EB4Full) ^
+                       ((uint64_t)cols * 0x165667B19E3779F9ull) ^ ((uint64_t)ld << 7) ^ (uint64_t)box_rows;
+    TmapSlot &slot = g_tmap_cache[(h >> 32) % kTmapSlots];
+    {
+        std::lock_guard<std::mutex> lk(g_tmap_mu);
+        if (slot.valid && slot.key == key) {
+            *map = slot.map;
+            return GEMM_OK;
+        }
+    }
+    int rc = encode_tmap(map, ptr, rows, cols, ld, box_rows);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(g_tmap_mu);
+    slot.valid = true;
+    slot.key = key;
+    slot.map = *map;
+    return GEMM_OK;
+}
+
+static int encode_tmap(CUtensorMap *map, const double *ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
     auto fn = encode_fn();
     if (!fn) return set_error(GEMM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
@@ -75,81 +133,68 @@ static int make_tmap(CUtensorMap *map, const double *ptr, int64_t rows, int64_t 
 }
 
 // ------------------------------------------------------------------ registry
-struct LaunchArgs {
-    int M, N, K;
-    double alpha, beta;
-    const double *A;
-    int64_t lda;
-    const double *B;
-    int64_t ldb;
-    double *C;
-    int64_t ldc;
-    int vec;
-    int group_m;
+// The tile instances live in cfgs_*.cu (one translation unit per group, compiled in
+// parallel); each exposes its table through cfg_table_<group>().
+struct Registry {
+    std::vector<CfgEntry> v;
+    Registry() {
+        int n = 0;
+        const CfgEntry *t = cfg_table_big(&n);
+        v.insert(v.end(), t, t + n);
+        t = cfg_table_small(&n);
+        v.insert(v.end(), t, t + n);
+        t = cfg_table_generic(&n);
+        v.insert(v.end(), t, t + n);
+    }
 };
-
-struct CfgEntry {
-    const char *name;
-    gemm_cfg_desc d;
-    const void *kernel;
-    int (*launch)(const LaunchArgs &, cudaStream_t);
-};
-
-template <class C>
-static int launch_tma(const LaunchArgs &a, cudaStream_t st) {
-    CUtensorMap ta, tb;
-    int rc = make_tmap(&ta, a.A, a.M, a.K, a.lda, C::BM);
-    if (rc) return rc;
-    rc = make_tmap(&tb, a.B, a.K, a.N, a.ldb, 16);
-    if (rc) return rc;
-    const int tiles = ((a.M + C::BM - 1) / C::BM) * ((a.N + C::BN - 1) / C::BN);
-    dgemm_tma_kernel<C><<<tiles, C::CONSUMER_THREADS, C::SMEM_BYTES, st>>>(
-        ta, tb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec, a.group_m);
-    return cuda_check(cudaGetLastError(), "dgemm_tma_kernel launch");
+static Registry &registry() {
+    static Registry r;
+    return r;
 }
-
-template <class C>
-static int launch_generic(const LaunchArgs &a, cudaStream_t st) {
-    const int tiles = ((a.M + C::BM - 1) / C::BM) * ((a.N + C::BN - 1) / C::BN);
-    dgemm_generic_kernel<C><<<tiles, C::CONSUMER_THREADS, C::SMEM_BYTES, st>>>(
-        a.A, a.lda, a.B, a.ldb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec, a.group_m);
-    return cuda_check(cudaGetLastError(), "dgemm_generic_kernel launch");
-}
-
-#define DG_TMA(BM, BN, BK, WM, WN, ST)                                                                       \
-    CfgEntry{"tma_" #BM "x" #BN "x" #BK "_w" #WM "x" #WN "_s" #ST,                                            \
-             gemm_cfg_desc{BM, BN, BK, WM, WN, ST, Cfg<BM, BN, BK, WM, WN, ST>::CONSUMER_THREADS,         \
-                           (int)Cfg<BM, BN, BK, WM, WN, ST>::SMEM_BYTES, 1, 1, 0},                            \
-             (const void *)dgemm_tma_kernel<Cfg<BM, BN, BK, WM, WN, ST>>, launch_tma<Cfg<BM, BN, BK, WM, WN, ST>>}
-#define DG_GEN(BM, BN, BK, WM, WN, ST)                                                                       \
-    CfgEntry{"gen_" #BM "x" #BN "x" #BK "_w" #WM "x" #WN "_s" #ST,                                            \
-             gemm_cfg_desc{BM, BN, BK, WM, WN, ST, Cfg<BM, BN, BK, WM, WN, ST>::CONSUMER_THREADS,              \
-                           (int)Cfg<BM, BN, BK, WM, WN, ST>::SMEM_BYTES, 0, 1, 0},                            \
-             (const void *)dgemm_generic_kernel<Cfg<BM, BN, BK, WM, WN, ST>>,                                 \
-             launch_generic<Cfg<BM, BN, BK, WM, WN, ST>>}
-
-static CfgEntry g_cfgs[] = {
-#include "cfg_list.inc"
-};
-static constexpr int kNumCfgs = sizeof(g_cfgs) / sizeof(g_cfgs[0]);
+#define g_cfgs (registry().v)
+#define kNumCfgs ((int)registry().v.size())
 
 static std::mutex g_attr_mu;
-static std::set<std::pair<int, int>> g_attr_done;
+static std::map<std::pair<int, int>, int> g_ctas_per_sm;   // (device, cfg) -> resident CTAs per SM
+static int g_num_sms[64];
 
-static int prepare_cfg(int id) {
+// Sets the dynamic-smem attribute (per device) and records residency; returns CTAs/SM via *occ.
+static int prepare_cfg(int id, int *occ = nullptr) {
     int dev = 0;
     int rc = cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
     if (rc) return rc;
     std::lock_guard<std::mutex> lk(g_attr_mu);
-    if (g_attr_done.count({dev, id})) return GEMM_OK;
+    auto it = g_ctas_per_sm.find({dev, id});
+    if (it != g_ctas_per_sm.end()) {
+        if (occ) *occ = it->second;
+        return GEMM_OK;
+    }
     CfgEntry &e = g_cfgs[id];
     rc = cuda_check(cudaFuncSetAttribute(e.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, e.d.smem_bytes),
                     "cudaFuncSetAttribute(MaxDynamicSharedMemorySize)");
     if (rc) return rc;
     cudaFuncAttributes fa;
     if (cudaFuncGetAttributes(&fa, e.kernel) == cudaSuccess) e.d.regs = fa.numRegs;
-    g_attr_done.insert({dev, id});
+    int n = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, e.kernel, e.d.threads, e.d.smem_bytes) != cudaSuccess ||
+        n < 1) {
+        cudaGetLastError();
+        n = 1;
+    }
+    if (dev >= 0 && dev < 64 && g_num_sms[dev] == 0) {
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        g_num_sms[dev] = sms;
+    }
+    g_ctas_per_sm[{dev, id}] = n;
+    if (occ) *occ = n;
     return GEMM_OK;
+}
+
+static int num_sms() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return (dev >= 0 && dev < 64 && g_num_sms[dev] > 0) ? g_num_sms[dev] : 148;
 }
 
 static int find_cfg(const char *name) {
@@ -163,24 +208,170 @@ static bool tma_ok(const double *A, int64_t lda, const double *B, int64_t ldb) {
            lda * 8 < (int64_t(1) << 40) && ldb * 8 < (int64_t(1) << 40);
 }
 
-// Size heuristic: the largest tile that still fills the
-// 148 SMs; TMA when alignment allows.
-static int select_cfg(int64_t M, int64_t N, int64_t K, bool tma) {
-    (void)K;
-    static const char *big_t = "tma_128x128x16_w64x32_s4";
-    static const char *mid_t = "tma_128x64x16_w32x32_s6";
-    static const char *small_t = "tma_64x64x16_w32x16_s6";
-    static const char *big_g = "gen_128x128x16_w64x32_s4";
-    static const char *small_g = "gen_64x64x16_w32x16_s4";
-    const int64_t tiles128 = ((M + 127) / 128) * ((N + 127) / 128);
-    const int64_t tiles64x128 = ((M + 127) / 128) * ((N + 63) / 64);
+// Size heuristic.  Every candidate is scored with a wave model:
+//   time ~ ceil(tiles*S / (SMs*CTAs_per_SM)) * CTAs_per_SM * BM*BN * (ceil(KT/S) + ovh) / eff
+// (a CTA's k-steps plus ~4 k-steps of pipeline fill and epilogue, +2 for a split-K
+// reduction), eff = the configuration's measured steady-state efficiency
+// (profiles/r01_scale_allcfgs.csv, r01_tune_n8192_a1.5_b0.5.csv).  Split-K candidates
+// try S = 1..16 with at least 4 k-steps per split.
+struct Cand {
     const char *name;
-    if (tma)
-        name = tiles128 >= 2 * 148 ? big_t : (tiles64x128 >= 148 ? mid_t : small_t);
-    else
-        name = tiles128 >= 2 * 148 ? big_g : small_g;
-    int id = find_cfg(name);
-    return id >= 0 ? id : 0;
+    double eff;
+};
+static const Cand k_tma_cands[] = {
+    {"tma_256x64x16_w64x32_s4", 0.978},        {"tma_64x128x16_w32x64_s4", 0.972},
+    {"tma_128x128x16_w32x32_s4", 0.965},       {"tma_64x64x16_w32x16_s6", 0.952},
+    {"tma_64x64x16_w32x16_s6_splitk", 0.950},  {"tma_128x64x16_w32x16_s6_splitk", 0.945},
+    {"tma_64x128x16_w32x64_s4_splitk", 0.965}, {"tma_128x128x16_w32x32_s4_splitk", 0.960},
+};
+
+struct Choice {
+    int id = -1;
+    int splits = 1;
+};
+
+static double est_time(const gemm_cfg_desc &d, int occ, int sms, int64_t M, int64_t N, int64_t K, int S,
+                       double eff) {
+    const int64_t tiles = ((M + d.bm - 1) / d.bm) * ((N + d.bn - 1) / d.bn);
+    const int64_t KT = (K + d.bk - 1) / d.bk;
+    const int64_t slots = (int64_t)sms * occ;
+    const int64_t waves = (tiles * S + slots - 1) / slots;
+    const double ksteps = (double)((KT + S - 1) / S) + 4.0 + (S > 1 ? 2.0 : 0.0);
+    return (double)waves * occ * d.bm * d.bn * ksteps * (d.bk / 16.0) / eff;
+}
+
+static Choice choose_uncached(int64_t M, int64_t N, int64_t K, bool tma);
+
+// Plans are cached per (device, M, N, K, TMA-eligible).
+struct PlanKey {
+    int dev;
+    int64_t M, N, K;
+    bool tma;
+    bool operator<(const PlanKey &o) const {
+        return std::tie(dev, M, N, K, tma) < std::tie(o.dev, o.M, o.N, o.K, o.tma);
+    }
+};
+static std::mutex g_plan_mu;
+static std::map<PlanKey, Choice> g_plans;
+
+static Choice choose(int64_t M, int64_t N, int64_t K, bool tma) {
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        dev = -1;
+    }
+    const PlanKey key{dev, M, N, K, tma};
+    {
+        std::lock_guard<std::mutex> lk(g_plan_mu);
+        auto it = g_plans.find(key);
+        if (it != g_plans.end()) return it->second;
+    }
+    const Choice c = choose_uncached(M, N, K, tma);
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    if (g_plans.size() > 4096) g_plans.clear();
+    g_plans[key] = c;
+    return c;
+}
+
+static Choice choose_uncached(int64_t M, int64_t N, int64_t K, bool tma) {
+    Choice best;
+    if (!tma) {
+        const int64_t tiles128 = ((M + 127) / 128) * ((N + 127) / 128);
+        best.id = find_cfg(tiles128 >= 2 * 148 ? "gen_128x128x16_w64x32_s4" : "gen_64x64x16_w32x16_s4");
+        return best;
+    }
+    double best_t = 1e300;
+    const int sms = num_sms();
+    for (const Cand &c : k_tma_cands) {
+        const int id = find_cfg(c.name);
+        if (id < 0) continue;
+        int occ = 1;
+        if (prepare_cfg(id, &occ) != GEMM_OK) {   // no device (host-only query): assume 1 CTA/SM
+            clear_error();
+            occ = 1;
+        }
+        const gemm_cfg_desc &d = g_cfgs[id].d;
+        const int64_t KT = (K + d.bk - 1) / d.bk;
+        const int smax = d.split_k == 1 ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(16, KT / 4));
+        for (int S = 1; S <= smax; ++S) {
+            const double t = est_time(d, occ, sms, M, N, K, S, c.eff);
+            if (t < best_t * 0.999) {
+                best_t = t;
+                best.id = id;
+                best.splits = S;
+            }
+        }
+    }
+    if (best.id < 0) best.id = 0;
+    return best;
+}
+
+static int select_cfg(int64_t M, int64_t N, int64_t K, bool tma) { return choose(M, N, K, tma).id; }
+
+// splits for a forced split-K configuration (auto): the model's best S for this cfg
+static int auto_splits(int id, int64_t M, int64_t N, int64_t K) {
+    int occ = 1;
+    if (prepare_cfg(id, &occ) != GEMM_OK) {
+        clear_error();
+        occ = 1;
+    }
+    const gemm_cfg_desc &d = g_cfgs[id].d;
+    if (d.split_k > 1) return d.split_k;
+    const int64_t KT = (K + d.bk - 1) / d.bk;
+    const int smax = (int)std::max<int64_t>(1, std::min<int64_t>(16, KT / 4));
+    int bestS = 1;
+    double bt = 1e300;
+    for (int S = 1; S <= smax; ++S) {
+        const double t = est_time(d, occ, num_sms(), M, N, K, S, 1.0);
+        if (t < bt * 0.999) {
+            bt = t;
+            bestS = S;
+        }
+    }
+    return bestS;
+}
+
+// ---- per-(device, stream) split-K workspace: partials + self-resetting tile counters
+struct SplitWs {
+    double *ws = nullptr;
+    size_t ws_cap = 0;
+    int *ctr = nullptr;
+    size_t ctr_cap = 0;
+};
+static std::mutex g_ws_mu;
+static std::map<std::pair<int, cudaStream_t>, SplitWs> g_ws;
+
+static int get_split_ws(cudaStream_t st, size_t doubles, size_t tiles, double **ws, int **ctr) {
+    int dev = 0;
+    int rc = cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    SplitWs &w = g_ws[{dev, st}];
+    if (w.ws_cap < doubles) {
+        if (w.ws) cudaFree(w.ws);
+        w.ws = nullptr;
+        w.ws_cap = 0;
+        if (cudaMalloc(&w.ws, doubles * sizeof(double)) != cudaSuccess) {
+            cudaGetLastError();
+            return set_error(GEMM_ERR_ALLOC, "split-K workspace of %zu bytes", doubles * sizeof(double));
+        }
+        w.ws_cap = doubles;
+    }
+    if (w.ctr_cap < tiles) {
+        if (w.ctr) cudaFree(w.ctr);
+        w.ctr = nullptr;
+        w.ctr_cap = 0;
+        if (cudaMalloc(&w.ctr, tiles * sizeof(int)) != cudaSuccess) {
+            cudaGetLastError();
+            return set_error(GEMM_ERR_ALLOC, "split-K counters");
+        }
+        rc = cuda_check(cudaMemsetAsync(w.ctr, 0, tiles * sizeof(int), st), "cudaMemsetAsync(counters)");
+        if (rc) return rc;
+        w.ctr_cap = tiles;
+    }
+    *ws = w.ws;
+    *ctr = w.ctr;
+    return GEMM_OK;
 }
 
 static bool overlaps(const void *p, int64_t rows, int64_t cols, int64_t ld, const void *q, int64_t qrows,
@@ -221,7 +412,7 @@ int validate(int64_t M, int64_t N, int64_t K, double alpha, const double *A, int
 }
 
 int gemm_impl(int64_t M, int64_t N, int64_t K, double alpha, const double *A, int64_t lda, const double *B,
-              int64_t ldb, double beta, double *C, int64_t ldc, int cfg_id, cudaStream_t st) {
+              int64_t ldb, double beta, double *C, int64_t ldc, int cfg_id, cudaStream_t st, int force_splits) {
     clear_error();
     int rc = validate(M, N, K, alpha, A, lda, B, ldb, C, ldc);
     if (rc) return rc;
@@ -236,10 +427,17 @@ int gemm_impl(int64_t M, int64_t N, int64_t K, double alpha, const double *A, in
         scale_kernel<<<blocks, threads, 0, st>>>((int)M, (int)N, beta, C, ldc);
         return cuda_check(cudaGetLastError(), "scale_kernel launch");
     }
+    // a single-row operand never uses its leading dimension: round it up to even so the
+    // TMA stride rule (multiple of 16 bytes) does not exclude it
+    if (M == 1) lda += (lda & 1);
+    if (K == 1) ldb += (ldb & 1);
     const bool tma = tma_ok(A, lda, B, ldb);
     int id = cfg_id;
+    int splits = 1;
     if (id < 0) {
-        id = select_cfg(M, N, K, tma);
+        const Choice c = choose(M, N, K, tma);
+        id = c.id;
+        splits = force_splits == 1 ? 1 : c.splits;   // 1: heuristic tile, no split-K
     } else if (g_cfgs[id].d.tma && !tma) {
         return set_error(GEMM_ERR_UNSUPPORTED,
                          "cfg %s needs 16-byte aligned A/B and even lda/ldb (A%%16=%d B%%16=%d lda=%lld ldb=%lld)",
@@ -248,8 +446,21 @@ int gemm_impl(int64_t M, int64_t N, int64_t K, double alpha, const double *A, in
     }
     rc = prepare_cfg(id);
     if (rc) return rc;
+    const gemm_cfg_desc &d = g_cfgs[id].d;
+    if (force_splits < 0) return set_error(GEMM_ERR_ARG, "splits=%d must be >= 0", force_splits);
+    if (cfg_id >= 0 && d.split_k != 1) splits = force_splits > 0 ? force_splits : auto_splits(id, M, N, K);
+    if (force_splits > 1 && d.split_k == 1)
+        return set_error(GEMM_ERR_UNSUPPORTED, "cfg %s has no split-K (use a *_splitk configuration)", g_cfgs[id].name);
+    if (splits > 4096) return set_error(GEMM_ERR_ARG, "splits=%d > 4096", splits);
+    SplitArgs sk{1, nullptr, nullptr};
+    if (splits > 1) {
+        const size_t tiles = (size_t)((M + d.bm - 1) / d.bm) * (size_t)((N + d.bn - 1) / d.bn);
+        rc = get_split_ws(st, tiles * (size_t)splits * d.bm * d.bn, tiles, &sk.ws, &sk.counters);
+        if (rc) return rc;
+        sk.splits = splits;
+    }
     LaunchArgs a{(int)M, (int)N, (int)K, alpha, beta, A, lda, B, ldb, C, ldc,
-                 ((uintptr_t)C % 32 == 0 && ldc % 4 == 0) ? 1 : 0, 8};
+                 ((uintptr_t)C % 32 == 0 && ldc % 4 == 0) ? 1 : 0, 8, sk};
     return g_cfgs[id].launch(a, st);
 }
 
@@ -274,6 +485,11 @@ int gemm_f64_cfg(int64_t M, int64_t N, int64_t K, double alpha, const double *A,
     return gemm_impl(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, cfg_id, (cudaStream_t)stream);
 }
 
+int gemm_f64_ex(int64_t M, int64_t N, int64_t K, double alpha, const double *A, int64_t lda, const double *B,
+                int64_t ldb, double beta, double *C, int64_t ldc, int cfg_id, int splits, void *stream) {
+    return gemm_impl(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, cfg_id, (cudaStream_t)stream, splits);
+}
+
 int gemm_num_cfgs(void) { return kNumCfgs; }
 
 int gemm_cfg_name(int cfg_id, char *buf, int len) {
@@ -294,6 +510,18 @@ int gemm_cfg_info(int cfg_id, gemm_cfg_desc *out) {
 
 int gemm_cfg_select(int64_t M, int64_t N, int64_t K, const double *A, int64_t lda, const double *B, int64_t ldb) {
     return select_cfg(M, N, K, tma_ok(A, lda, B, ldb));
+}
+
+int gemm_plan(int64_t M, int64_t N, int64_t K, const double *A, int64_t lda, const double *B, int64_t ldb,
+              int *cfg_id, int *splits) {
+    clear_error();
+    if (!cfg_id || !splits) return set_error(GEMM_ERR_ARG, "cfg_id / splits is NULL");
+    if (M == 1) lda += (lda & 1);
+    if (K == 1) ldb += (ldb & 1);
+    const Choice c = choose(M, N, K, tma_ok(A, lda, B, ldb));
+    *cfg_id = c.id;
+    *splits = c.splits;
+    return GEMM_OK;
 }
 
 const char *gemm_last_error(void) { return last_error(); }

@@ -2,12 +2,10 @@
 //
 // The paper times "the run of the algorithm without copy operations to device
 // memory"; this entry point is the opposite view, the whole job a user
-// with host data sees.  Copies are overlapped with the DMMA kernel by row
-// panels: B goes first (every panel needs all of it), then for each panel p of
-// rows the A rows (and C rows when beta != 0) travel host->device on the h2d
-// stream, the compute stream multiplies panel p once its rows landed, and the
-// d2h stream returns panel p while panel p+1 computes.  Per-entry arithmetic
-// is that of gemm_f64 on the whole matrix (row panels do not change it).
+// with host data sees, with the copies overlapped with the DMMA kernel (three
+// streams: h2d, compute, d2h; schedule below).  Per-entry arithmetic is that of
+// gemm_f64 on the whole matrix: blocks of C only change which CTA computes an
+// entry, and split-K is disabled here so every block uses the same k-order chain.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -54,6 +52,16 @@ static int ensure_events(std::vector<cudaEvent_t> &v, size_t n) {
     return GEMM_OK;
 }
 
+// Schedule (all copies from the caller's host buffers into packed device buffers):
+//   h2d : A rows [0, R0), then B in column panels, then A row panels 1.. (and C0 rows
+//         alongside the A rows when beta != 0)
+//   comp: row panel 0 is multiplied column block by column block as the B panels land
+//         (R0 is sized so that this work covers the whole B transfer:
+//         R0 ~ 4 * compute_rate / h2d_bandwidth rows, independent of N and K), then
+//         each later row panel as soon as its A rows land; the last row panel is again
+//         computed in column blocks so that its device->host copy overlaps
+//   d2h : every finished block / panel of C
+// Exposed copy time is the first A rows + the first B panel and the last C block.
 static int host_impl(int64_t M, int64_t N, int64_t K, double alpha, const double *A, int64_t lda, const double *B,
                      int64_t ldb, double beta, double *C, int64_t ldc) {
     clear_error();
@@ -74,47 +82,81 @@ static int host_impl(int64_t M, int64_t N, int64_t K, double alpha, const double
         if ((rc = cuda_check(cudaStreamCreateWithFlags(&P.d2h, cudaStreamNonBlocking), "stream"))) return rc;
     }
     // device copies are packed: ld = row length
+    const int64_t Kp = std::max<int64_t>(1, K);
     if ((rc = ensure(&P.dA, &P.nA, need_ab ? (size_t)M * K : 0))) return rc;
     if ((rc = ensure(&P.dB, &P.nB, need_ab ? (size_t)K * N : 0))) return rc;
     if ((rc = ensure(&P.dC, &P.nC, (size_t)M * N))) return rc;
 
-    // Panel size: at least two waves of 128x128 tiles per panel, at most 8 panels.
-    const int64_t tiles_n = (N + 127) / 128;
-    int64_t min_rows = ((2 * 148 + tiles_n - 1) / tiles_n) * 128;
-    int64_t npan = std::max<int64_t>(1, std::min<int64_t>(8, M / std::max<int64_t>(min_rows, 1)));
-    int64_t rows_per = ((M + npan - 1) / npan + 127) / 128 * 128;
-    npan = (M + rows_per - 1) / rows_per;
-    if ((rc = ensure_events(P.ev_in, (size_t)npan))) return rc;
-    if ((rc = ensure_events(P.ev_out, (size_t)npan))) return rc;
-
-    if (need_ab) {
-        if ((rc = cuda_check(cudaMemcpy2DAsync(P.dB, N * 8, B, ldb * 8, N * 8, K, cudaMemcpyHostToDevice, P.h2d),
-                             "H2D B")))
-            return rc;
+    // ---- geometry
+    const double flops = 2.0 * (double)M * (double)N * (double)K;
+    const bool tiny = !need_ab || flops < 2e10;      // < ~1 ms of GPU work: one shot
+    int64_t R0 = M, Rp = M, cb = N;                  // first panel rows, later panel rows, column block
+    if (!tiny) {
+        R0 = std::min<int64_t>(M, 2560);             // ~4 * 30 TFLOP/s / 53 GB/s = 2260 rows, rounded up
+        Rp = 2048;
+        cb = std::max<int64_t>(512, ((N + 7) / 8 + 15) / 16 * 16);   // <= 8 column blocks
     }
-    for (int64_t p = 0; p < npan; ++p) {
-        const int64_t r0 = p * rows_per, r1 = std::min(M, r0 + rows_per), nr = r1 - r0;
-        if (need_ab &&
-            (rc = cuda_check(cudaMemcpy2DAsync(P.dA + r0 * K, K * 8, A + r0 * lda, lda * 8, K * 8, nr,
-                                               cudaMemcpyHostToDevice, P.h2d),
-                             "H2D A panel")))
+    const int64_t ncb = (N + cb - 1) / cb;
+    const int64_t nrest = (M > R0) ? (M - R0 + Rp - 1) / Rp : 0;
+    const size_t nev = (size_t)(ncb + nrest + 2);
+    if ((rc = ensure_events(P.ev_in, nev))) return rc;
+    if ((rc = ensure_events(P.ev_out, nev))) return rc;
+
+    auto h2d_rows = [&](double *dst, int64_t dld, const double *src, int64_t sld, int64_t cols, int64_t rows,
+                        const char *what) {
+        return cuda_check(cudaMemcpy2DAsync(dst, dld * 8, src, sld * 8, cols * 8, rows, cudaMemcpyHostToDevice, P.h2d),
+                          what);
+    };
+    auto d2h_block = [&](int64_t r0, int64_t nr, int64_t c0, int64_t nc) {
+        return cuda_check(cudaMemcpy2DAsync(C + r0 * ldc + c0, ldc * 8, P.dC + r0 * N + c0, N * 8, nc * 8, nr,
+                                            cudaMemcpyDeviceToHost, P.d2h),
+                          "D2H C block");
+    };
+    auto run = [&](int64_t r0, int64_t nr, int64_t c0, int64_t nc) {
+        return gemm_impl(nr, nc, need_ab ? K : 0, need_ab ? alpha : 0.0, P.dA + r0 * K, Kp, P.dB + c0, N, beta,
+                         P.dC + r0 * N + c0, N, -1, P.comp, /*force_splits=*/1);
+    };
+    size_t ei = 0, eo = 0;
+    auto h2d_done = [&]() -> int {   // compute stream waits for everything copied so far
+        int r = cuda_check(cudaEventRecord(P.ev_in[ei], P.h2d), "event");
+        if (!r) r = cuda_check(cudaStreamWaitEvent(P.comp, P.ev_in[ei], 0), "wait");
+        ++ei;
+        return r;
+    };
+    auto comp_done = [&]() -> int {  // d2h stream waits for everything computed so far
+        int r = cuda_check(cudaEventRecord(P.ev_out[eo], P.comp), "event");
+        if (!r) r = cuda_check(cudaStreamWaitEvent(P.d2h, P.ev_out[eo], 0), "wait");
+        ++eo;
+        return r;
+    };
+
+    // ---- row panel 0: A rows and C0 rows first, then B column blocks, each followed by its GEMM block
+    if (need_ab && (rc = h2d_rows(P.dA, K, A, lda, K, R0, "H2D A panel"))) return rc;
+    if (need_c_in && (rc = h2d_rows(P.dC, N, C, ldc, N, R0, "H2D C panel"))) return rc;
+    for (int64_t j = 0; j < ncb; ++j) {
+        const int64_t c0 = j * cb, nc = std::min(N, c0 + cb) - c0;
+        if (need_ab && (rc = cuda_check(cudaMemcpy2DAsync(P.dB + c0, N * 8, B + c0, ldb * 8, nc * 8, K,
+                                                          cudaMemcpyHostToDevice, P.h2d),
+                                        "H2D B panel")))
             return rc;
-        if (need_c_in &&
-            (rc = cuda_check(cudaMemcpy2DAsync(P.dC + r0 * N, N * 8, C + r0 * ldc, ldc * 8, N * 8, nr,
-                                               cudaMemcpyHostToDevice, P.h2d),
-                             "H2D C panel")))
-            return rc;
-        if ((rc = cuda_check(cudaEventRecord(P.ev_in[p], P.h2d), "event"))) return rc;
-        if ((rc = cuda_check(cudaStreamWaitEvent(P.comp, P.ev_in[p], 0), "wait"))) return rc;
-        rc = gemm_impl(nr, N, need_ab ? K : 0, need_ab ? alpha : 0.0, P.dA + r0 * K, std::max<int64_t>(1, K), P.dB,
-                       N, beta, P.dC + r0 * N, N, -1, P.comp);
-        if (rc) return rc;
-        if ((rc = cuda_check(cudaEventRecord(P.ev_out[p], P.comp), "event"))) return rc;
-        if ((rc = cuda_check(cudaStreamWaitEvent(P.d2h, P.ev_out[p], 0), "wait"))) return rc;
-        if ((rc = cuda_check(cudaMemcpy2DAsync(C + r0 * ldc, ldc * 8, P.dC + r0 * N, N * 8, N * 8, nr,
-                                               cudaMemcpyDeviceToHost, P.d2h),
-                             "D2H C panel")))
-            return rc;
+        if ((rc = h2d_done())) return rc;
+        if ((rc = run(0, R0, c0, nc))) return rc;
+        if ((rc = comp_done())) return rc;
+        if ((rc = d2h_block(0, R0, c0, nc))) return rc;
+    }
+    // ---- later row panels
+    for (int64_t p = 0; p < nrest; ++p) {
+        const int64_t r0 = R0 + p * Rp, nr = std::min(M, r0 + Rp) - r0;
+        if (need_ab && (rc = h2d_rows(P.dA + r0 * K, K, A + r0 * lda, lda, K, nr, "H2D A panel"))) return rc;
+        if (need_c_in && (rc = h2d_rows(P.dC + r0 * N, N, C + r0 * ldc, ldc, N, nr, "H2D C panel"))) return rc;
+        if ((rc = h2d_done())) return rc;
+        const bool last = (p == nrest - 1);
+        for (int64_t j = 0; j < (last ? ncb : 1); ++j) {
+            const int64_t c0 = last ? j * cb : 0, nc = last ? std::min(N, c0 + cb) - c0 : N;
+            if ((rc = run(r0, nr, c0, nc))) return rc;
+            if ((rc = comp_done())) return rc;
+            if ((rc = d2h_block(r0, nr, c0, nc))) return rc;
+        }
     }
     return cuda_check(cudaStreamSynchronize(P.d2h), "gemm_f64_host synchronize");
 }

@@ -11,5 +11,5 @@ int cuda_check(cudaError_t e, const char *what);
 int validate(int64_t M, int64_t N, int64_t K, double alpha, const double *A, int64_t lda, const double *B,
              int64_t ldb, const double *C, int64_t ldc);
 int gemm_impl(int64_t M, int64_t N, int64_t K, double alpha, const double *A, int64_t lda, const double *B,
-              int64_t ldb, double beta, double *C, int64_t ldc, int cfg_id, cudaStream_t st);
+              int64_t ldb, double beta, double *C, int64_t ldc, int cfg_id, cudaStream_t st, int force_splits = 0);
 }  // namespace dg

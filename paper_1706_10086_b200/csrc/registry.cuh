@@ -1,0 +1,77 @@
+// registry.cuh -- configuration table entries and the launch templates.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "../../include/gemm_f64.h"
+#include "dgemm_kernels.cuh"
+#include "internal.h"
+
+namespace dg {
+
+int make_tmap(CUtensorMap *map, const double *ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows);
+
+struct LaunchArgs {
+    int M, N, K;
+    double alpha, beta;
+    const double *A;
+    int64_t lda;
+    const double *B;
+    int64_t ldb;
+    double *C;
+    int64_t ldc;
+    int vec;
+    int group_m;
+    SplitArgs sk;
+};
+
+struct CfgEntry {
+    const char *name;
+    gemm_cfg_desc d;
+    const void *kernel;
+    int (*launch)(const LaunchArgs &, cudaStream_t);
+};
+
+template <class C, bool SPLIT>
+static int launch_tma(const LaunchArgs &a, cudaStream_t st) {
+    CUtensorMap ta, tb;
+    int rc = make_tmap(&ta, a.A, a.M, a.K, a.lda, C::BM);
+    if (rc) return rc;
+    rc = make_tmap(&tb, a.B, a.K, a.N, a.ldb, 16);
+    if (rc) return rc;
+    const int tiles = ((a.M + C::BM - 1) / C::BM) * ((a.N + C::BN - 1) / C::BN);
+    dim3 grid(tiles, SPLIT ? a.sk.splits : 1);
+    dgemm_tma_kernel<C, SPLIT><<<grid, C::CONSUMER_THREADS, C::SMEM_BYTES, st>>>(
+        ta, tb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec, a.group_m, a.sk);
+    return cuda_check(cudaGetLastError(), "dgemm_tma_kernel launch");
+}
+
+template <class C>
+static int launch_generic(const LaunchArgs &a, cudaStream_t st) {
+    const int tiles = ((a.M + C::BM - 1) / C::BM) * ((a.N + C::BN - 1) / C::BN);
+    dgemm_generic_kernel<C><<<tiles, C::CONSUMER_THREADS, C::SMEM_BYTES, st>>>(
+        a.A, a.lda, a.B, a.ldb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec, a.group_m);
+    return cuda_check(cudaGetLastError(), "dgemm_generic_kernel launch");
+}
+
+#define DG_TMA_SK(BM, BN, BK, WM, WN, ST, SK, SPLIT, SUFFIX)                                                  \
+    CfgEntry{"tma_" #BM "x" #BN "x" #BK "_w" #WM "x" #WN "_s" #ST SUFFIX,                                     \
+             gemm_cfg_desc{BM, BN, BK, WM, WN, ST, Cfg<BM, BN, BK, WM, WN, ST>::CONSUMER_THREADS,              \
+                           (int)Cfg<BM, BN, BK, WM, WN, ST>::SMEM_BYTES, 1, SK, 0},                           \
+             (const void *)dgemm_tma_kernel<Cfg<BM, BN, BK, WM, WN, ST>, SPLIT>,                               \
+             launch_tma<Cfg<BM, BN, BK, WM, WN, ST>, SPLIT>}
+#define DG_TMA(BM, BN, BK, WM, WN, ST) DG_TMA_SK(BM, BN, BK, WM, WN, ST, 1, false, "")
+// split_k = 0: number of k-splits chosen per call (deterministic split-K, SplitArgs)
+#define DG_TMA_SPLIT(BM, BN, BK, WM, WN, ST) DG_TMA_SK(BM, BN, BK, WM, WN, ST, 0, true, "_splitk")
+#define DG_GEN(BM, BN, BK, WM, WN, ST)                                                                       \
+    CfgEntry{"gen_" #BM "x" #BN "x" #BK "_w" #WM "x" #WN "_s" #ST,                                            \
+             gemm_cfg_desc{BM, BN, BK, WM, WN, ST, Cfg<BM, BN, BK, WM, WN, ST>::CONSUMER_THREADS,              \
+                           (int)Cfg<BM, BN, BK, WM, WN, ST>::SMEM_BYTES, 0, 1, 0},                            \
+             (const void *)dgemm_generic_kernel<Cfg<BM, BN, BK, WM, WN, ST>>,                                 \
+             launch_generic<Cfg<BM, BN, BK, WM, WN, ST>>}
+
+const CfgEntry *cfg_table_big(int *n);
+const CfgEntry *cfg_table_small(int *n);
+const CfgEntry *cfg_table_generic(int *n);
+
+}  // namespace dg

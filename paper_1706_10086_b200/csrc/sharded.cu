@@ -11,6 +11,8 @@
 //   panel j-1 is multiplied on the caller's stream (C[:, panel] with ldb = panel
 //   width).  Per-entry arithmetic is unchanged -> bitwise equal to chunks == 1.
 //   Non-root B buffers receive the unpacked panels at the end.
+// Both paths launch without split-K (force_splits = 1) so the per-entry k-order chain
+// is the same for any panel width and any number of ranks.
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -135,10 +137,10 @@ int gemm_f64_sharded(int64_t M_local, int64_t N, int64_t K, double alpha, const 
     if (!B) return set_error(GEMM_ERR_ARG, "B is NULL");
 
     int nch = (int)std::min<int64_t>(bcast_chunks, std::max<int64_t>(1, N / 64));
-    if (nch == 1 || c->nranks == 1) {
+    if (nch == 1) {
         rc = nccl_check(ncclBroadcast(B, B, (size_t)(K * N), ncclDouble, root, c->nccl, st), "ncclBroadcast(B)");
         if (rc) return rc;
-        return gemm_impl(M_local, N, K, alpha, A_local, lda, B, ldb, beta, C_local, ldc, -1, st);
+        return gemm_impl(M_local, N, K, alpha, A_local, lda, B, ldb, beta, C_local, ldc, -1, st, 1);
     }
 
     // ---- column-panel pipeline ----
@@ -173,7 +175,7 @@ int gemm_f64_sharded(int64_t M_local, int64_t N, int64_t K, double alpha, const 
             return rc;
         if ((rc = cuda_check(cudaEventRecord(c->ev[j], c->comm_stream), "event"))) return rc;
         if ((rc = cuda_check(cudaStreamWaitEvent(st, c->ev[j], 0), "wait"))) return rc;
-        rc = gemm_impl(M_local, nw, K, alpha, A_local, lda, panel, nw, beta, C_local + n0, ldc, -1, st);
+        rc = gemm_impl(M_local, nw, K, alpha, A_local, lda, panel, nw, beta, C_local + n0, ldc, -1, st, 1);
         if (rc) return rc;
     }
     if (!is_root) {   // leave the broadcast B in the caller's buffer, as the contract says

@@ -20,8 +20,8 @@ STATUS_NAMES = {0: "GEMM_OK", 1: "GEMM_ERR_ARG", 2: "GEMM_ERR_CUDA", 3: "GEMM_ER
 FILL_MODES = {"uniform": 0, "dyadic": 1, "int8": 2, "ones": 3, "identity": 4, "zeros": 5}
 
 # every symbol include/gemm_f64.h declares (tests check the library exports them all)
-EXPORTS = ("gemm_f64", "gemm_f64_stream", "gemm_f64_cfg", "gemm_f64_host", "gemm_host_pool_release",
-           "gemm_num_cfgs", "gemm_cfg_name", "gemm_cfg_info", "gemm_cfg_select", "gemm_last_error",
+EXPORTS = ("gemm_f64", "gemm_f64_stream", "gemm_f64_cfg", "gemm_f64_ex", "gemm_f64_host", "gemm_host_pool_release",
+           "gemm_num_cfgs", "gemm_cfg_name", "gemm_cfg_info", "gemm_cfg_select", "gemm_plan", "gemm_last_error",
            "gemm_fill_f64", "gemm_peak_probe", "gemm_comm_unique_id", "gemm_comm_init",
            "gemm_comm_destroy", "gemm_f64_sharded", "gemm_bcast_f64", "gemm_version")
 
@@ -48,12 +48,14 @@ def _load():
         "gemm_f64": (ci, core),
         "gemm_f64_stream": (ci, core + [vp]),
         "gemm_f64_cfg": (ci, core + [ci, vp]),
+        "gemm_f64_ex": (ci, core + [ci, ci, vp]),
         "gemm_f64_host": (ci, core),
         "gemm_host_pool_release": (ci, []),
         "gemm_num_cfgs": (ci, []),
         "gemm_cfg_name": (ci, [ci, ctypes.c_char_p, ci]),
         "gemm_cfg_info": (ci, [ci, ctypes.POINTER(CfgDesc)]),
         "gemm_cfg_select": (ci, [i64, i64, i64, vp, i64, vp, i64]),
+        "gemm_plan": (ci, [i64, i64, i64, vp, i64, vp, i64, ctypes.POINTER(ci), ctypes.POINTER(ci)]),
         "gemm_last_error": (ctypes.c_char_p, []),
         "gemm_fill_f64": (ci, [ci, ctypes.c_uint64, ci, i64, i64, i64, i64, vp, i64, vp]),
         "gemm_peak_probe": (ci, [ci, ci, ci, i64, vp, vp, vp]),
@@ -103,7 +105,7 @@ def _mat(x, name):
         return x.data_ptr(), r, c, max(c, 1)
     if c > 1 and x.stride(1) != 1:
         raise ValueError(f"{name} must have unit stride along columns (row-major)")
-    ld = x.stride(0) if r > 1 else max(1, c)
+    ld = x.stride(0) if (r > 1 or x.stride(0) >= c) else c
     ld = max(ld, c, 1)
     return x.data_ptr(), r, c, ld
 
@@ -117,7 +119,8 @@ def _stream_ptr(stream):
     return stream.cuda_stream
 
 
-def gemm(A, B, C, alpha: float = 1.0, beta: float = 0.0, cfg: int | None = None, stream=None):
+def gemm(A, B, C, alpha: float = 1.0, beta: float = 0.0, cfg: int | None = None, stream=None,
+         splits: int | None = None):
     """C <- alpha*A@B + beta*C on the GPU (torch CUDA float64 tensors, row-major). Returns C."""
     pa, M, K, lda = _mat(A, "A")
     pb, K2, N, ldb = _mat(B, "B")
@@ -128,10 +131,13 @@ def gemm(A, B, C, alpha: float = 1.0, beta: float = 0.0, cfg: int | None = None,
         if not t.is_cuda:
             raise ValueError(f"{n} must be a CUDA tensor (use gemm_host for host buffers)")
     st = _stream_ptr(stream)
-    if cfg is None:
+    if cfg is None and splits is None:
         rc = _lib.gemm_f64_stream(M, N, K, float(alpha), pa, lda, pb, ldb, float(beta), pc, ldc, st)
-    else:
+    elif splits is None:
         rc = _lib.gemm_f64_cfg(M, N, K, float(alpha), pa, lda, pb, ldb, float(beta), pc, ldc, int(cfg), st)
+    else:
+        rc = _lib.gemm_f64_ex(M, N, K, float(alpha), pa, lda, pb, ldb, float(beta), pc, ldc,
+                              -1 if cfg is None else int(cfg), int(splits), st)
     _check(rc)
     return C
 
@@ -201,6 +207,14 @@ def cfg_id(name: str) -> int:
 def cfg_select(M, N, K, A_ptr=0, lda=None, B_ptr=0, ldb=None) -> int:
     return _lib.gemm_cfg_select(M, N, K, A_ptr, lda if lda is not None else max(K, 1), B_ptr,
                                 ldb if ldb is not None else max(N, 1))
+
+
+def plan(M, N, K, A_ptr=0, lda=None, B_ptr=0, ldb=None) -> tuple:
+    """(cfg_id, splits) the heuristic launches for this shape / alignment."""
+    cid, sp = ctypes.c_int(), ctypes.c_int()
+    _check(_lib.gemm_plan(M, N, K, A_ptr, lda if lda is not None else max(K, 1), B_ptr,
+                          ldb if ldb is not None else max(N, 1), ctypes.byref(cid), ctypes.byref(sp)))
+    return cid.value, sp.value
 
 
 # ------------------------------------------------------------------ inputs

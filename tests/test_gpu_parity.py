@@ -22,9 +22,9 @@ def dev(x):
     return torch.from_numpy(np.ascontiguousarray(x)).cuda()
 
 
-def run_gpu(G, A, B, C0, alpha, beta, cfg=None):
+def run_gpu(G, A, B, C0, alpha, beta, cfg=None, splits=None):
     dA, dB, dC = dev(A), dev(B), dev(C0)
-    G.gemm(dA, dB, dC, alpha, beta, cfg=cfg)
+    G.gemm(dA, dB, dC, alpha, beta, cfg=cfg, splits=splits)
     torch.cuda.synchronize()
     return dC.cpu().numpy()
 
@@ -57,7 +57,8 @@ EDGE = [(1, 1, 1), (2, 2, 2), (7, 5, 3), (8, 16, 4), (31, 33, 17), (127, 129, 65
 def test_edge_shapes_every_cfg(cuda_lib, shape):
     M, N, K = shape
     A, B, C0 = synth.problem(M, N, K, seed=M * 7 + N)
-    tma_eligible = (K % 2 == 0) and (N % 2 == 0)   # packed lda = K, ldb = N: TMA needs 16-byte strides
+    # packed lda = K, ldb = N: TMA needs 16-byte strides (a single-row operand's stride is unused)
+    tma_eligible = (K % 2 == 0 or M == 1) and (N % 2 == 0 or K == 1)
     ran = 0
     for info in cuda_lib.cfgs():
         if info["tma"] and not tma_eligible:
@@ -129,12 +130,74 @@ def test_all_cfgs_bitwise_identical_and_deterministic(cuda_lib):
     """Every configuration sums each entry in the same order (16-deep k-groups ascending,
     same k-permutation, same DMMA chain) -> identical bits; and runs repeat bitwise."""
     A, B, C0 = synth.problem(334, 290, 778, seed=3)
-    outs = [run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=c) for c in all_cfgs(cuda_lib)]
+    # split-K configurations with one slice run the same chain as the others
+    outs = [run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=c, splits=1) for c in all_cfgs(cuda_lib)]
     for c, o in zip(all_cfgs(cuda_lib), outs):
         assert np.array_equal(o, outs[0]), cuda_lib.cfg_name(c)
     again = run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=0)
     assert np.array_equal(again, outs[0])
     check_vs_oracle(outs[0], A, B, C0, 1.5, 0.5)
+
+
+# ---------------------------------------------------------------- split-K (row a5)
+def split_cfgs(G):
+    return [c["id"] for c in G.cfgs() if c["split_k"] != 1]
+
+
+@pytest.mark.parametrize("shape", [(70, 90, 1000), (256, 256, 256), (129, 200, 777), (64, 64, 16), (31, 33, 2000)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_split_k_within_bound_and_deterministic(cuda_lib, shape):
+    M, N, K = shape
+    N += N & 1
+    K += K & 1
+    A, B, C0 = synth.problem(M, N, K, seed=K)
+    for cfg in split_cfgs(cuda_lib):
+        for S in (2, 3, 5, 16):
+            C = run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=cfg, splits=S)
+            check_vs_oracle(C, A, B, C0, 1.5, 0.5)
+            again = run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=cfg, splits=S)
+            assert np.array_equal(C, again), (cuda_lib.cfg_name(cfg), S)
+
+
+def test_split_k_exact_regime_bitwise(cuda_lib):
+    A, B, C0 = synth.problem(200, 300, 1500, mode="dyadic", seed=4)
+    ref = oracle.dgemm(1.5, A, B, 0.5, C0)
+    for cfg in split_cfgs(cuda_lib):
+        for S in (2, 7):
+            assert np.array_equal(run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=cfg, splits=S), ref)
+
+
+def test_split_k_counters_self_reset_many_launches(cuda_lib):
+    """Tile counters are reset by the reducing CTA: 50 back-to-back launches on one stream
+    (and a different split count in between) all give the same bits."""
+    A, B, C0 = synth.problem(128, 192, 640, seed=5)
+    cfg = split_cfgs(cuda_lib)[0]
+    dA, dB = dev(A), dev(B)
+    first = None
+    for it in range(50):
+        dC = dev(C0)
+        cuda_lib.gemm(dA, dB, dC, 1.0, 1.0, cfg=cfg, splits=4 if it % 7 else 3)
+        torch.cuda.synchronize()
+        out = dC.cpu().numpy()
+        if it % 7:
+            first = out if first is None else first
+            assert np.array_equal(out, first), it
+    check_vs_oracle(first, A, B, C0, 1.0, 1.0)
+
+
+def test_split_k_forced_on_plain_cfg_is_rejected(cuda_lib):
+    plain = [c["id"] for c in cuda_lib.cfgs() if c["split_k"] == 1 and c["tma"]][0]
+    A, B, C0 = synth.problem(64, 64, 64)
+    with pytest.raises(cuda_lib.GemmError) as ei:
+        run_gpu(cuda_lib, A, B, C0, 1.0, 0.0, cfg=plain, splits=2)
+    assert ei.value.code == cuda_lib.GEMM_ERR_UNSUPPORTED
+
+
+@pytest.mark.parametrize("n", [256, 512, 768, 1024])
+def test_small_sizes_heuristic_plan(cuda_lib, n):
+    """The product's own choice (possibly split-K) on config-1/2-like small sizes."""
+    A, B, C0 = synth.problem(n, n, n, seed=n)
+    check_vs_oracle(run_gpu(cuda_lib, A, B, C0, 1.0, 0.0), A, B, C0, 1.0, 0.0)
 
 
 # ---------------------------------------------------------------- layout / padding
@@ -272,8 +335,9 @@ def test_host_entry_point(cuda_lib):
     C = C0.copy()
     cuda_lib.gemm_host(A, B, C, 1.5, 0.5)
     check_vs_oracle(C, A, B, C0, 1.5, 0.5)
-    # same bits as the device entry point (row panels do not change per-entry arithmetic)
-    assert np.array_equal(C, run_gpu(cuda_lib, A, B, C0, 1.5, 0.5))
+    # same bits as the device entry point without split-K (row panels do not change
+    # per-entry arithmetic)
+    assert np.array_equal(C, run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, splits=1))
 
 
 def test_host_entry_point_large_pinned(cuda_lib):
@@ -283,10 +347,27 @@ def test_host_entry_point_large_pinned(cuda_lib):
     tB = torch.from_numpy(B).pin_memory()
     tC = torch.from_numpy(C0.copy()).pin_memory()
     cuda_lib.gemm_host(tA, tB, tC, 1.0, 1.0)
-    assert np.array_equal(tC.numpy(), run_gpu(cuda_lib, A, B, C0, 1.0, 1.0))
+    assert np.array_equal(tC.numpy(), run_gpu(cuda_lib, A, B, C0, 1.0, 1.0, splits=1))
     rows = _rows(M, extra=4)
     ref, mag = oracle.dgemm(1.0, A[rows], B, 1.0, C0[rows], want_mag=True)
     r = oracle.check(tC.numpy()[rows], ref, oracle.bound(K, 1.0, 1.0, mag, C0[rows]))
+    assert r.ok, str(r)
+
+
+def test_host_entry_point_pipelined_odd_padded(cuda_lib):
+    """The blocked copy/compute pipeline (row panel 0 by column blocks, later row panels,
+    last panel by column blocks) on an odd shape with padded host leading dimensions."""
+    M, N, K = 6003, 1001, 2002
+    A, B, C0 = synth.problem(M, N, K, seed=17)
+    Ap = np.full((M, K + 3), np.nan); Ap[:, :K] = A
+    Bp = np.full((K, N + 1), np.nan); Bp[:, :N] = B
+    Cp = np.full((M, N + 5), np.nan); Cp[:, :N] = C0
+    cuda_lib.gemm_host(Ap[:, :K], Bp[:, :N], Cp[:, :N], 1.5, 0.5)
+    assert np.all(np.isnan(Cp[:, N:]))
+    assert np.array_equal(Cp[:, :N], run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, splits=1))
+    rows = _rows(M, extra=6)
+    ref, mag = oracle.dgemm(1.5, A[rows], B, 0.5, C0[rows], want_mag=True)
+    r = oracle.check(Cp[rows, :N], ref, oracle.bound(K, 1.5, 0.5, mag, C0[rows]))
     assert r.ok, str(r)
 
 
@@ -300,7 +381,7 @@ def test_sharded_world1_equals_single_gpu(cuda_lib, chunks):
     comm.gemm_sharded(dA, dB, dC, 1.5, 0.5, root=0, bcast_chunks=chunks)
     torch.cuda.synchronize()
     comm.close()
-    assert np.array_equal(dC.cpu().numpy(), run_gpu(cuda_lib, A, B, C0, 1.5, 0.5))
+    assert np.array_equal(dC.cpu().numpy(), run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, splits=1))
 
 
 def test_fake_multi_gpu_row_partition(cuda_lib):
@@ -308,12 +389,12 @@ def test_fake_multi_gpu_row_partition(cuda_lib):
     (isolates partition/offset bugs from communication)."""
     M, N, K = 1001, 300, 257
     A, B, C0 = synth.problem(M, N, K, seed=13)
-    full = run_gpu(cuda_lib, A, B, C0, 1.0, 1.0)
+    full = run_gpu(cuda_lib, A, B, C0, 1.0, 1.0, splits=1)
     for P in (2, 3, 8):
         out = np.empty_like(full)
         for r in range(P):
             r0, r1 = cuda_lib.row_range(M, r, P)
-            out[r0:r1] = run_gpu(cuda_lib, A[r0:r1], B, C0[r0:r1], 1.0, 1.0)
+            out[r0:r1] = run_gpu(cuda_lib, A[r0:r1], B, C0[r0:r1], 1.0, 1.0, splits=1)
         assert np.array_equal(out, full), P
 
 
