@@ -14,6 +14,8 @@ static const CfgEntry k_table[] = {
     DG_TMA(128, 128, 16, 32, 32, 6),
     DG_TMA(256, 64, 16, 64, 32, 4),
     DG_TMA(256, 64, 16, 32, 32, 4),
+    DG_TMA_XP(256, 64, 16, 64, 32, 4),
+    DG_TMA_XP(128, 128, 16, 64, 32, 4),
 };
 
 const CfgEntry *cfg_table_big(int *n) {

@@ -9,6 +9,8 @@ static const CfgEntry k_table[] = {
     DG_TMA(128, 64, 16, 32, 32, 6),
     DG_TMA(128, 64, 16, 32, 16, 6),
     DG_TMA(64, 128, 16, 32, 64, 4),
+    DG_TMA_XP(64, 128, 16, 32, 64, 4),
+    DG_TMA_XP(64, 64, 16, 32, 16, 6),
     DG_TMA(64, 128, 16, 32, 32, 6),
     DG_TMA(64, 128, 16, 16, 32, 6),
     DG_TMA(64, 64, 16, 64, 32, 6),

@@ -127,6 +127,40 @@ __device__ __forceinline__ void mma_stage(uint32_t sA, uint32_t sB, const FragOf
     }
 }
 
+// The same tile multiply split into "halves" (one k-group half p: 2 MMA slices) so that a
+// caller can keep the next half's fragments in flight while the current half's DMMAs
+// issue -- across the stage boundary too (cross-stage prefetch, XP kernels).
+template <class C>
+struct Frag {
+    double a[C::MB][2];
+    double b[C::NP][2][2];
+};
+
+template <class C>
+__device__ __forceinline__ void load_half(uint32_t sA, uint32_t sB, int h, const FragOffsets<C> &fo, Frag<C> &f) {
+    const int kg = h >> 1, p = h & 1;
+#pragma unroll
+    for (int mb = 0; mb < C::MB; ++mb) lds_v2(sA + kg * C::A_SUB + mb * 1024 + fo.a[p], f.a[mb][0], f.a[mb][1]);
+#pragma unroll
+    for (int np = 0; np < C::NP; ++np)
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+            lds_v2(sB + kg * C::B_KG + np * C::B_BOX + fo.b[p][s], f.b[np][s][0], f.b[np][s][1]);
+}
+
+template <class C>
+__device__ __forceinline__ void mma_half(const Frag<C> &f, double (&acc)[C::MB][C::NP][2][2]) {
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+#pragma unroll
+        for (int mb = 0; mb < C::MB; ++mb)
+#pragma unroll
+            for (int np = 0; np < C::NP; ++np)
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+                    dmma_m8n8k4(acc[mb][np][j][0], acc[mb][np][j][1], f.a[mb][s], f.b[np][s][j]);
+}
+
 // Epilogue (row a4): C = alpha*acc + beta*C, each C element read (beta != 0) and written once.
 // Thread (g, t) of an (m-block, n-pair) owns row g and the 4 contiguous columns 4t..4t+3:
 // acc[mb][np][j][i] is real column 4t + 2i + j of the n-pair.
@@ -264,7 +298,10 @@ __device__ __forceinline__ bool split_reduce(double (&acc)[C::MB][C::NP][2][2], 
 
 // SPLIT = false instantiations carry no split-K code (the reduction's registers would
 // otherwise raise the 256x64/64x32 kernel from 199 to 255 registers).
-template <class C, bool SPLIT>
+// XP = true: cross-stage fragment prefetch -- the first half of stage i+1 is loaded (after
+// its full-barrier wait) before the last half of stage i is multiplied, so the DMMA pipe
+// does not drain at stage boundaries.
+template <class C, bool SPLIT, bool XP>
 __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
     dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
                      int N, int K, double alpha, double beta, double *__restrict__ Cm, int64_t ldc, int vec,
@@ -314,21 +351,58 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
 #pragma unroll
             for (int j = 0; j < 2; ++j) acc[mb][np][j][0] = acc[mb][np][j][1] = 0.0;
 
-    for (int i = 0; i < NK; ++i) {
-        const int s = i % C::STAGES;
-        if (producer && i > 0) {
-            const int in = i - 1 + C::STAGES;   // refill the slot released at i-1
-            if (in < NK) {
-                const int sp = (i - 1) % C::STAGES;
-                mbar_wait(&empty[sp], ((i - 1) / C::STAGES) & 1);
-                tma_issue_stage<C>(base_ptr + sp * C::STAGE_BYTES, &tmA, &tmB, &full[sp], m0, n0, kt0 + in, pol);
+    if constexpr (!XP) {
+        for (int i = 0; i < NK; ++i) {
+            const int s = i % C::STAGES;
+            if (producer && i > 0) {
+                const int in = i - 1 + C::STAGES;   // refill the slot released at i-1
+                if (in < NK) {
+                    const int sp = (i - 1) % C::STAGES;
+                    mbar_wait(&empty[sp], ((i - 1) / C::STAGES) & 1);
+                    tma_issue_stage<C>(base_ptr + sp * C::STAGE_BYTES, &tmA, &tmB, &full[sp], m0, n0, kt0 + in,
+                                       pol);
+                }
             }
+            mbar_wait(&full[s], (i / C::STAGES) & 1);
+            const uint32_t sA = base + s * C::STAGE_BYTES;
+            mma_stage<C>(sA, sA + C::A_BYTES, fo, acc);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
         }
-        mbar_wait(&full[s], (i / C::STAGES) & 1);
-        const uint32_t sA = base + s * C::STAGE_BYTES;
-        mma_stage<C>(sA, sA + C::A_BYTES, fo, acc);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
+    } else {
+        constexpr int H = 2 * C::KG;   // halves per stage (even: half 0 of every stage uses f[0])
+        Frag<C> f[2];
+        if (NK > 0) {
+            mbar_wait(&full[0], 0);
+            load_half<C>(base, base + C::A_BYTES, 0, fo, f[0]);
+        }
+        for (int i = 0; i < NK; ++i) {
+            const int s = i % C::STAGES;
+            if (producer && i > 0) {
+                const int in = i - 1 + C::STAGES;
+                if (in < NK) {
+                    const int sp = (i - 1) % C::STAGES;
+                    mbar_wait(&empty[sp], ((i - 1) / C::STAGES) & 1);
+                    tma_issue_stage<C>(base_ptr + sp * C::STAGE_BYTES, &tmA, &tmB, &full[sp], m0, n0, kt0 + in,
+                                       pol);
+                }
+            }
+            const uint32_t sA = base + s * C::STAGE_BYTES;
+#pragma unroll
+            for (int h = 0; h < H; ++h) {
+                if (h + 1 < H) {
+                    load_half<C>(sA, sA + C::A_BYTES, h + 1, fo, f[(h + 1) & 1]);
+                } else if (i + 1 < NK) {
+                    const int s1 = (i + 1) % C::STAGES;
+                    mbar_wait(&full[s1], ((i + 1) / C::STAGES) & 1);
+                    const uint32_t sA1 = base + s1 * C::STAGE_BYTES;
+                    load_half<C>(sA1, sA1 + C::A_BYTES, 0, fo, f[0]);
+                }
+                mma_half<C>(f[h & 1], acc);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
     }
     if constexpr (SPLIT) {
         if (!split_reduce<C>(acc, sk, blockIdx.x, split, warp, lane)) return;

@@ -219,7 +219,8 @@ struct Cand {
     double eff;
 };
 static const Cand k_tma_cands[] = {
-    {"tma_256x64x16_w64x32_s4", 0.978},        {"tma_64x128x16_w32x64_s4", 0.972},
+    {"tma_256x64x16_w64x32_s4_xp", 0.981},     {"tma_128x128x16_w64x32_s4_xp", 0.979},
+    {"tma_64x128x16_w32x64_s4", 0.972},
     {"tma_128x128x16_w32x32_s4", 0.965},       {"tma_64x64x16_w32x16_s6", 0.952},
     {"tma_64x64x16_w32x16_s6_splitk", 0.950},  {"tma_128x64x16_w32x16_s6_splitk", 0.945},
     {"tma_64x128x16_w32x64_s4_splitk", 0.965}, {"tma_128x128x16_w32x32_s4_splitk", 0.960},

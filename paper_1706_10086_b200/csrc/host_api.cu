@@ -98,7 +98,9 @@ static int host_impl(int64_t M, int64_t N, int64_t K, double alpha, const double
     }
     const int64_t ncb = (N + cb - 1) / cb;
     const int64_t nrest = (M > R0) ? (M - R0 + Rp - 1) / Rp : 0;
-    const size_t nev = (size_t)(ncb + nrest + 2);
+    // events: one per column block of panel 0, one per later panel, one per column block
+    // of the last panel (h2d_done / comp_done each use at most this many)
+    const size_t nev = (size_t)(2 * ncb + nrest + 2);
     if ((rc = ensure_events(P.ev_in, nev))) return rc;
     if ((rc = ensure_events(P.ev_out, nev))) return rc;
 
@@ -118,12 +120,14 @@ static int host_impl(int64_t M, int64_t N, int64_t K, double alpha, const double
     };
     size_t ei = 0, eo = 0;
     auto h2d_done = [&]() -> int {   // compute stream waits for everything copied so far
+        if (ei >= P.ev_in.size()) return set_error(GEMM_ERR_CUDA, "internal: h2d event pool exhausted");
         int r = cuda_check(cudaEventRecord(P.ev_in[ei], P.h2d), "event");
         if (!r) r = cuda_check(cudaStreamWaitEvent(P.comp, P.ev_in[ei], 0), "wait");
         ++ei;
         return r;
     };
     auto comp_done = [&]() -> int {  // d2h stream waits for everything computed so far
+        if (eo >= P.ev_out.size()) return set_error(GEMM_ERR_CUDA, "internal: d2h event pool exhausted");
         int r = cuda_check(cudaEventRecord(P.ev_out[eo], P.comp), "event");
         if (!r) r = cuda_check(cudaStreamWaitEvent(P.d2h, P.ev_out[eo], 0), "wait");
         ++eo;

@@ -32,7 +32,7 @@ struct CfgEntry {
     int (*launch)(const LaunchArgs &, cudaStream_t);
 };
 
-template <class C, bool SPLIT>
+template <class C, bool SPLIT, bool XP>
 static int launch_tma(const LaunchArgs &a, cudaStream_t st) {
     CUtensorMap ta, tb;
     int rc = make_tmap(&ta, a.A, a.M, a.K, a.lda, C::BM);
@@ -41,7 +41,7 @@ static int launch_tma(const LaunchArgs &a, cudaStream_t st) {
     if (rc) return rc;
     const int tiles = ((a.M + C::BM - 1) / C::BM) * ((a.N + C::BN - 1) / C::BN);
     dim3 grid(tiles, SPLIT ? a.sk.splits : 1);
-    dgemm_tma_kernel<C, SPLIT><<<grid, C::CONSUMER_THREADS, C::SMEM_BYTES, st>>>(
+    dgemm_tma_kernel<C, SPLIT, XP><<<grid, C::CONSUMER_THREADS, C::SMEM_BYTES, st>>>(
         ta, tb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec, a.group_m, a.sk);
     return cuda_check(cudaGetLastError(), "dgemm_tma_kernel launch");
 }
@@ -54,15 +54,17 @@ static int launch_generic(const LaunchArgs &a, cudaStream_t st) {
     return cuda_check(cudaGetLastError(), "dgemm_generic_kernel launch");
 }
 
-#define DG_TMA_SK(BM, BN, BK, WM, WN, ST, SK, SPLIT, SUFFIX)                                                  \
+#define DG_TMA_SK(BM, BN, BK, WM, WN, ST, SK, SPLIT, XP, SUFFIX)                                              \
     CfgEntry{"tma_" #BM "x" #BN "x" #BK "_w" #WM "x" #WN "_s" #ST SUFFIX,                                     \
              gemm_cfg_desc{BM, BN, BK, WM, WN, ST, Cfg<BM, BN, BK, WM, WN, ST>::CONSUMER_THREADS,              \
                            (int)Cfg<BM, BN, BK, WM, WN, ST>::SMEM_BYTES, 1, SK, 0},                           \
-             (const void *)dgemm_tma_kernel<Cfg<BM, BN, BK, WM, WN, ST>, SPLIT>,                               \
-             launch_tma<Cfg<BM, BN, BK, WM, WN, ST>, SPLIT>}
-#define DG_TMA(BM, BN, BK, WM, WN, ST) DG_TMA_SK(BM, BN, BK, WM, WN, ST, 1, false, "")
+             (const void *)dgemm_tma_kernel<Cfg<BM, BN, BK, WM, WN, ST>, SPLIT, XP>,                           \
+             launch_tma<Cfg<BM, BN, BK, WM, WN, ST>, SPLIT, XP>}
+#define DG_TMA(BM, BN, BK, WM, WN, ST) DG_TMA_SK(BM, BN, BK, WM, WN, ST, 1, false, false, "")
 // split_k = 0: number of k-splits chosen per call (deterministic split-K, SplitArgs)
-#define DG_TMA_SPLIT(BM, BN, BK, WM, WN, ST) DG_TMA_SK(BM, BN, BK, WM, WN, ST, 0, true, "_splitk")
+#define DG_TMA_SPLIT(BM, BN, BK, WM, WN, ST) DG_TMA_SK(BM, BN, BK, WM, WN, ST, 0, true, false, "_splitk")
+// cross-stage fragment prefetch variant
+#define DG_TMA_XP(BM, BN, BK, WM, WN, ST) DG_TMA_SK(BM, BN, BK, WM, WN, ST, 1, false, true, "_xp")
 #define DG_GEN(BM, BN, BK, WM, WN, ST)                                                                       \
     CfgEntry{"gen_" #BM "x" #BN "x" #BK "_w" #WM "x" #WN "_s" #ST,                                            \
              gemm_cfg_desc{BM, BN, BK, WM, WN, ST, Cfg<BM, BN, BK, WM, WN, ST>::CONSUMER_THREADS,              \
