@@ -264,8 +264,12 @@ def main():
     G.fill(dC, "uniform", 1706, 2, rows=M, row0=r0)
     stream = torch.cuda.current_stream()
     comm = G.Comm(rank, world) if world > 1 else None
-    cfg = a.cfg if a.cfg >= 0 else G.cfg_select(Ml, N, K, dA.data_ptr(), K, dB.data_ptr(), N)
-    cfg_name = G.cfg_name(cfg)
+    # the product's own plan (heuristic entry point) unless a configuration is forced
+    cfg = a.cfg if a.cfg >= 0 else None
+    plan_cfg, plan_splits = G.plan(Ml, N, K, dA.data_ptr(), K, dB.data_ptr(), N)
+    cfg_name = G.cfg_name(cfg if cfg is not None else plan_cfg)
+    if cfg is None and plan_splits > 1:
+        cfg_name += f" (split-K x{plan_splits})"
 
     def step(evs=None):
         if comm is not None:

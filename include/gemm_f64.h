@@ -140,6 +140,16 @@ GEMM_API int gemm_cfg_select(int64_t M, int64_t N, int64_t K, const double *A, i
 GEMM_API int gemm_plan(int64_t M, int64_t N, int64_t K, const double *A, int64_t lda,
               const double *B, int64_t ldb, int *cfg_id, int *splits);
 
+/* Auto-tuner hooks (the paper's per-architecture tuning, §2.3, as a
+ * persisted per-shape table).  gemm_plan_set pins the plan the heuristic entry
+ * points use for (M, N, K, TMA-eligible) on the current device; gemm_plan_clear
+ * forgets all pinned and cached plans; gemm_tune_load reads a text table with
+ * lines "M N K tma cfg_name splits" ('#' comments), pinning each, and writes the
+ * number of entries loaded to *n_loaded (may be NULL). */
+GEMM_API int gemm_plan_set(int64_t M, int64_t N, int64_t K, int tma, int cfg_id, int splits);
+GEMM_API int gemm_plan_clear(void);
+GEMM_API int gemm_tune_load(const char *path, int *n_loaded);
+
 /* Thread-local message for the last non-OK return on this thread. */
 GEMM_API const char *gemm_last_error(void);
 

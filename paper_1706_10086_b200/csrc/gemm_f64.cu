@@ -513,6 +513,69 @@ int gemm_cfg_select(int64_t M, int64_t N, int64_t K, const double *A, int64_t ld
     return select_cfg(M, N, K, tma_ok(A, lda, B, ldb));
 }
 
+int gemm_plan_set(int64_t M, int64_t N, int64_t K, int tma, int cfg_id, int splits) {
+    clear_error();
+    if (M < 0 || N < 0 || K < 0) return set_error(GEMM_ERR_ARG, "negative shape");
+    if (cfg_id < 0 || cfg_id >= kNumCfgs) return set_error(GEMM_ERR_ARG, "cfg_id=%d out of range", cfg_id);
+    if (splits < 1 || splits > 4096) return set_error(GEMM_ERR_ARG, "splits=%d must be in [1, 4096]", splits);
+    if (splits > 1 && g_cfgs[cfg_id].d.split_k == 1)
+        return set_error(GEMM_ERR_ARG, "cfg %s has no split-K", g_cfgs[cfg_id].name);
+    if (g_cfgs[cfg_id].d.tma && !tma)
+        return set_error(GEMM_ERR_ARG, "cfg %s is a TMA configuration but tma=0", g_cfgs[cfg_id].name);
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        dev = -1;
+    }
+    Choice c;
+    c.id = cfg_id;
+    c.splits = splits;
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    g_plans[PlanKey{dev, M, N, K, tma != 0}] = c;
+    return GEMM_OK;
+}
+
+int gemm_plan_clear(void) {
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    g_plans.clear();
+    return GEMM_OK;
+}
+
+int gemm_tune_load(const char *path, int *n_loaded) {
+    clear_error();
+    if (n_loaded) *n_loaded = 0;
+    if (!path) return set_error(GEMM_ERR_ARG, "path is NULL");
+    FILE *f = fopen(path, "r");
+    if (!f) return set_error(GEMM_ERR_ARG, "cannot open tuning table %s", path);
+    char line[512];
+    int n = 0, lineno = 0;
+    while (fgets(line, sizeof(line), f)) {
+        ++lineno;
+        if (line[0] == '#' || line[0] == '\n') continue;
+        long long M, N, K;
+        int tma, splits;
+        char name[128];
+        if (sscanf(line, "%lld %lld %lld %d %127s %d", &M, &N, &K, &tma, name, &splits) != 6) {
+            fclose(f);
+            return set_error(GEMM_ERR_ARG, "%s:%d: expected 'M N K tma cfg_name splits'", path, lineno);
+        }
+        const int id = find_cfg(name);
+        if (id < 0) {
+            fclose(f);
+            return set_error(GEMM_ERR_ARG, "%s:%d: unknown configuration %s", path, lineno, name);
+        }
+        int rc = gemm_plan_set(M, N, K, tma, id, splits);
+        if (rc) {
+            fclose(f);
+            return rc;
+        }
+        ++n;
+        if (n_loaded) *n_loaded = n;
+    }
+    fclose(f);
+    return GEMM_OK;
+}
+
 int gemm_plan(int64_t M, int64_t N, int64_t K, const double *A, int64_t lda, const double *B, int64_t ldb,
               int *cfg_id, int *splits) {
     clear_error();

@@ -21,7 +21,8 @@ FILL_MODES = {"uniform": 0, "dyadic": 1, "int8": 2, "ones": 3, "identity": 4, "z
 
 # every symbol include/gemm_f64.h declares (tests check the library exports them all)
 EXPORTS = ("gemm_f64", "gemm_f64_stream", "gemm_f64_cfg", "gemm_f64_ex", "gemm_f64_host", "gemm_host_pool_release",
-           "gemm_num_cfgs", "gemm_cfg_name", "gemm_cfg_info", "gemm_cfg_select", "gemm_plan", "gemm_last_error",
+           "gemm_num_cfgs", "gemm_cfg_name", "gemm_cfg_info", "gemm_cfg_select", "gemm_plan", "gemm_plan_set",
+           "gemm_plan_clear", "gemm_tune_load", "gemm_last_error",
            "gemm_fill_f64", "gemm_peak_probe", "gemm_comm_unique_id", "gemm_comm_init",
            "gemm_comm_destroy", "gemm_f64_sharded", "gemm_bcast_f64", "gemm_version")
 
@@ -56,6 +57,9 @@ def _load():
         "gemm_cfg_info": (ci, [ci, ctypes.POINTER(CfgDesc)]),
         "gemm_cfg_select": (ci, [i64, i64, i64, vp, i64, vp, i64]),
         "gemm_plan": (ci, [i64, i64, i64, vp, i64, vp, i64, ctypes.POINTER(ci), ctypes.POINTER(ci)]),
+        "gemm_plan_set": (ci, [i64, i64, i64, ci, ci, ci]),
+        "gemm_plan_clear": (ci, []),
+        "gemm_tune_load": (ci, [ctypes.c_char_p, ctypes.POINTER(ci)]),
         "gemm_last_error": (ctypes.c_char_p, []),
         "gemm_fill_f64": (ci, [ci, ctypes.c_uint64, ci, i64, i64, i64, i64, vp, i64, vp]),
         "gemm_peak_probe": (ci, [ci, ci, ci, i64, vp, vp, vp]),
@@ -215,6 +219,22 @@ def plan(M, N, K, A_ptr=0, lda=None, B_ptr=0, ldb=None) -> tuple:
     _check(_lib.gemm_plan(M, N, K, A_ptr, lda if lda is not None else max(K, 1), B_ptr,
                           ldb if ldb is not None else max(N, 1), ctypes.byref(cid), ctypes.byref(sp)))
     return cid.value, sp.value
+
+
+def plan_set(M, N, K, tma: bool, cfg: int, splits: int = 1):
+    """Pin the plan used for (M, N, K, TMA-eligible) on the current device."""
+    _check(_lib.gemm_plan_set(M, N, K, int(bool(tma)), int(cfg), int(splits)))
+
+
+def plan_clear():
+    _check(_lib.gemm_plan_clear())
+
+
+def tune_load(path: str) -> int:
+    """Load a persisted tuning table (lines "M N K tma cfg_name splits"); returns entries loaded."""
+    n = ctypes.c_int()
+    _check(_lib.gemm_tune_load(os.fsencode(path), ctypes.byref(n)))
+    return n.value
 
 
 # ------------------------------------------------------------------ inputs

@@ -82,6 +82,9 @@ def raw_bits(seed: int, mat: int, rows: int, cols: int, row0: int = 0, nrows: in
         return _mix(_base(seed, mat) + ctr * _GAMMA)
 
 
+_CHUNK = 1 << 18   # elements per generation block (cache-resident temporaries)
+
+
 def matrix(mode: str, seed: int, mat: int, rows: int, cols: int,
            row0: int = 0, nrows: int | None = None) -> np.ndarray:
     """Rows [row0, row0+nrows) of the logical rows x cols matrix, C-contiguous float64."""
@@ -89,6 +92,18 @@ def matrix(mode: str, seed: int, mat: int, rows: int, cols: int,
         raise ValueError(f"unknown mode {mode!r}; expected one of {MODES}")
     if nrows is None:
         nrows = rows - row0
+    if mode in ("uniform", "dyadic", "int8") and nrows * cols > 2 * _CHUNK and cols > 0:
+        # same values, generated in row blocks whose temporaries stay in cache
+        out = np.empty((nrows, cols), dtype=np.float64)
+        step = max(1, _CHUNK // cols)
+        for r in range(0, nrows, step):
+            n = min(step, nrows - r)
+            out[r:r + n] = _matrix_block(mode, seed, mat, rows, cols, row0 + r, n)
+        return out
+    return _matrix_block(mode, seed, mat, rows, cols, row0, nrows)
+
+
+def _matrix_block(mode, seed, mat, rows, cols, row0, nrows):
     if mode == "ones":
         return np.ones((nrows, cols), dtype=np.float64)
     if mode == "zeros":

@@ -280,3 +280,10 @@ def test_synth_dyadic_values():
     assert np.all(X * 256 == np.round(X * 256)) and X.min() >= -1 and X.max() <= 1
     Y = synth.matrix("int8", 2, 0, 100, 100)
     assert np.all(Y == np.round(Y)) and Y.min() == -8 and Y.max() == 8
+
+
+def test_synth_chunked_generation_is_identical():
+    rows, cols = 700, 1000    # > 2 chunks of 2^18 elements
+    for mode in ("uniform", "dyadic", "int8"):
+        assert np.array_equal(synth.matrix(mode, 5, 1, rows, cols),
+                              synth._matrix_block(mode, 5, 1, rows, cols, 0, rows))
