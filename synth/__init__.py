@@ -69,15 +69,20 @@ def _base(seed: int, mat: int) -> np.uint64:
         return _mix(z)[0]
 
 
-def raw_bits(seed: int, mat: int, rows: int, cols: int, row0: int = 0, nrows: int | None = None) -> np.ndarray:
-    """The raw 64-bit counter stream r(i, j) for rows [row0, row0+nrows)."""
+def raw_bits(seed: int, mat: int, rows: int, cols: int, row0: int = 0, nrows: int | None = None,
+             col0: int = 0, ncols: int | None = None) -> np.ndarray:
+    """The raw 64-bit counter stream r(i, j) for rows [row0, row0+nrows), columns [col0, col0+ncols)."""
     if nrows is None:
         nrows = rows - row0
+    if ncols is None:
+        ncols = cols - col0
     if nrows < 0 or row0 < 0 or row0 + nrows > rows:
         raise ValueError(f"row slab [{row0},{row0 + nrows}) outside [0,{rows})")
+    if ncols < 0 or col0 < 0 or col0 + ncols > cols:
+        raise ValueError(f"column slab [{col0},{col0 + ncols}) outside [0,{cols})")
     with np.errstate(over="ignore"):
         i = np.arange(row0, row0 + nrows, dtype=np.uint64)[:, None]
-        j = np.arange(cols, dtype=np.uint64)[None, :]
+        j = np.arange(col0, col0 + ncols, dtype=np.uint64)[None, :]
         ctr = i * np.uint64(cols) + j + np.uint64(1)
         return _mix(_base(seed, mat) + ctr * _GAMMA)
 
@@ -86,35 +91,40 @@ _CHUNK = 1 << 18   # elements per generation block (cache-resident temporaries)
 
 
 def matrix(mode: str, seed: int, mat: int, rows: int, cols: int,
-           row0: int = 0, nrows: int | None = None) -> np.ndarray:
-    """Rows [row0, row0+nrows) of the logical rows x cols matrix, C-contiguous float64."""
+           row0: int = 0, nrows: int | None = None, col0: int = 0, ncols: int | None = None) -> np.ndarray:
+    """Block [row0, row0+nrows) x [col0, col0+ncols) of the logical rows x cols matrix
+    (default: whole rows), C-contiguous float64."""
     if mode not in MODE_ID:
         raise ValueError(f"unknown mode {mode!r}; expected one of {MODES}")
     if nrows is None:
         nrows = rows - row0
-    if mode in ("uniform", "dyadic", "int8") and nrows * cols > 2 * _CHUNK and cols > 0:
+    if ncols is None:
+        ncols = cols - col0
+    if mode in ("uniform", "dyadic", "int8") and nrows * ncols > 2 * _CHUNK and ncols > 0:
         # same values, generated in row blocks whose temporaries stay in cache
-        out = np.empty((nrows, cols), dtype=np.float64)
-        step = max(1, _CHUNK // cols)
+        out = np.empty((nrows, ncols), dtype=np.float64)
+        step = max(1, _CHUNK // ncols)
         for r in range(0, nrows, step):
             n = min(step, nrows - r)
-            out[r:r + n] = _matrix_block(mode, seed, mat, rows, cols, row0 + r, n)
+            out[r:r + n] = _matrix_block(mode, seed, mat, rows, cols, row0 + r, n, col0, ncols)
         return out
-    return _matrix_block(mode, seed, mat, rows, cols, row0, nrows)
+    return _matrix_block(mode, seed, mat, rows, cols, row0, nrows, col0, ncols)
 
 
-def _matrix_block(mode, seed, mat, rows, cols, row0, nrows):
+def _matrix_block(mode, seed, mat, rows, cols, row0, nrows, col0=0, ncols=None):
+    if ncols is None:
+        ncols = cols - col0
     if mode == "ones":
-        return np.ones((nrows, cols), dtype=np.float64)
+        return np.ones((nrows, ncols), dtype=np.float64)
     if mode == "zeros":
-        return np.zeros((nrows, cols), dtype=np.float64)
+        return np.zeros((nrows, ncols), dtype=np.float64)
     if mode == "identity":
-        out = np.zeros((nrows, cols), dtype=np.float64)
+        out = np.zeros((nrows, ncols), dtype=np.float64)
         for r in range(nrows):
-            if row0 + r < cols:
-                out[r, row0 + r] = 1.0
+            if col0 <= row0 + r < col0 + ncols:
+                out[r, row0 + r - col0] = 1.0
         return out
-    r = raw_bits(seed, mat, rows, cols, row0, nrows) >> np.uint64(11)
+    r = raw_bits(seed, mat, rows, cols, row0, nrows, col0, ncols) >> np.uint64(11)
     if mode == "uniform":
         return 2.0 * (r.astype(np.float64) * 2.0 ** -53) - 1.0
     if mode == "dyadic":

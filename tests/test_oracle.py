@@ -287,3 +287,10 @@ def test_synth_chunked_generation_is_identical():
     for mode in ("uniform", "dyadic", "int8"):
         assert np.array_equal(synth.matrix(mode, 5, 1, rows, cols),
                               synth._matrix_block(mode, 5, 1, rows, cols, 0, rows))
+
+
+def test_synth_column_block_consistency():
+    full = synth.matrix("uniform", 3, 1, 40, 57)
+    assert np.array_equal(full[5:17, 20:41], synth.matrix("uniform", 3, 1, 40, 57, row0=5, nrows=12, col0=20, ncols=21))
+    eye = synth.matrix("identity", 0, 0, 9, 9)
+    assert np.array_equal(eye[2:7, 3:8], synth.matrix("identity", 0, 0, 9, 9, row0=2, nrows=5, col0=3, ncols=5))

@@ -82,15 +82,21 @@ class Problem:
         G.fill(self.C, "uniform", self.seed, 2)
 
     def parity(self, cfg, alpha, beta, rows, splits=None):
+        """Sampled rows (all columns, or a 512-column block when K*N is huge) vs the oracle."""
         self.reset_c()
         G.gemm(self.A, self.B, self.C, alpha, beta, cfg=cfg, splits=splits)
         torch.cuda.synchronize()
-        if self._B_host is None:
-            self._B_host = synth.matrix("uniform", self.seed, 1, self.K, self.N)
+        c0, nc = 0, self.N
+        if self.K * self.N > (1 << 28):
+            nc = min(512, self.N)
+            c0 = int(np.random.default_rng(self.N).integers(0, self.N - nc + 1))
+        if self._B_host is None or self._B_host[0] != (c0, nc):
+            self._B_host = ((c0, nc), synth.matrix("uniform", self.seed, 1, self.K, self.N, col0=c0, ncols=nc))
         A_r = np.vstack([synth.matrix("uniform", self.seed, 0, self.M, self.K, row0=r, nrows=1) for r in rows])
-        C0_r = np.vstack([synth.matrix("uniform", self.seed, 2, self.M, self.N, row0=r, nrows=1) for r in rows])
-        ref, mag = oracle.dgemm(alpha, A_r, self._B_host, beta, C0_r, want_mag=True)
-        got = self.C[torch.tensor(rows, device="cuda")].cpu().numpy()
+        C0_r = np.vstack([synth.matrix("uniform", self.seed, 2, self.M, self.N, row0=r, nrows=1, col0=c0, ncols=nc)
+                          for r in rows])
+        ref, mag = oracle.dgemm(alpha, A_r, self._B_host[1], beta, C0_r, want_mag=True)
+        got = self.C[torch.tensor(rows, device="cuda")][:, c0:c0 + nc].cpu().numpy()
         res = oracle.check(got, ref, oracle.bound(self.K, alpha, beta, mag, C0_r))
         return res
 
@@ -153,21 +159,32 @@ def tune(a):
             print(",".join(map(str, r)), flush=True)
 
 
+def _shapes(a):
+    if a.shapes:
+        return [tuple(int(v) for v in item.split("x")) for item in a.shapes.split(",")]
+    if a.grid:
+        lo, hi, step = (int(v) for v in a.grid.split(":"))
+        return [(n, n, n) for n in range(lo, hi + 1, step)]
+    return [(n, n, n) for n in (int(x) for x in a.sizes.split(","))]
+
+
 def scale(a):
+    """Heuristic plan per shape (the product's choice), or every TMA configuration."""
     with open(a.out, "w", newline="") as f:
         w = csv.writer(f)
         w.writerow(HEADER)
-        for n in [int(x) for x in a.sizes.split(",")]:
-            P = Problem(n, n, n)
-            heur = G.cfg_select(n, n, n, P.A.data_ptr(), n, P.B.data_ptr(), n)
-            cands = [heur] if not a.all_cfgs else [c["id"] for c in G.cfgs() if c["tma"]]
+        for (m, n, k) in _shapes(a):
+            P = Problem(m, n, k)
+            heur, hs = G.plan(m, n, k, P.A.data_ptr(), k, P.B.data_ptr(), n)
+            cands = [None] if not a.all_cfgs else [c["id"] for c in G.cfgs() if c["tma"]]
             for cfg in cands:
-                res = P.parity(cfg, a.alpha, a.beta, sample_rows(n, extra=2))
+                res = P.parity(cfg, a.alpha, a.beta, sample_rows(m, extra=2))
                 if not res.ok:
-                    print(f"PARITY FAIL n={n} {G.cfg_name(cfg)}: {res}", flush=True)
+                    print(f"PARITY FAIL {m}x{n}x{k} {cfg}: {res}", flush=True)
                     continue
                 tb, tm, mhz, pw = P.time(cfg, a.alpha, a.beta, a.reps)
-                r = row(P, cfg, a.alpha, a.beta, tb, tm, mhz, pw, res.max_ratio, cfg == heur)
+                r = row(P, heur if cfg is None else cfg, a.alpha, a.beta, tb, tm, mhz, pw, res.max_ratio,
+                        cfg is None or cfg == heur, hs if cfg is None else 1)
                 w.writerow(r)
                 f.flush()
                 print(",".join(map(str, r)), flush=True)
@@ -222,6 +239,8 @@ def main():
     ap.add_argument("--sizes", default="1024,2048,4096,8192,16384")
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--all-cfgs", action="store_true")
+    ap.add_argument("--shapes", default=None, help="comma list of MxNxK")
+    ap.add_argument("--grid", default=None, help="lo:hi:step square sizes (the paper's N=1024..20480, dN=1024)")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     if a.alpha is None:
