@@ -99,6 +99,20 @@ GEMM_API int gemm_f64_ex(int64_t M, int64_t N, int64_t K, double alpha,
                 const double *A, int64_t lda, const double *B, int64_t ldb,
                 double beta, double *C, int64_t ldc, int cfg_id, int splits, void *cuda_stream);
 
+/* Single precision (the paper's second precision): C = alpha*A*B + beta*C on
+ * row-major FP32 device buffers, computed on the tensor cores with the 3xTF32 split
+ * (x = hi + lo, A_lo*B_hi + A_hi*B_lo + A_hi*B_hi accumulated in FP32 in TMEM by
+ * tcgen05.mma kind::tf32).  Accuracy is FP32-class; the acceptance bound used by the
+ * tests is DESIGN.md reading R16.  Any alignment (4-byte) and leading dimension: A and B
+ * are split into library workspace first (per stream).  Same argument rules and BLAS
+ * special cases as gemm_f64. */
+GEMM_API int gemm_f32(int64_t M, int64_t N, int64_t K, float alpha,
+             const float *A, int64_t lda, const float *B, int64_t ldb,
+             float beta, float *C, int64_t ldc);
+GEMM_API int gemm_f32_stream(int64_t M, int64_t N, int64_t K, float alpha,
+                    const float *A, int64_t lda, const float *B, int64_t ldb,
+                    float beta, float *C, int64_t ldc, void *cuda_stream);
+
 /* Host-buffer entry point ("the call a user makes" with host data): A, B, C are
  * HOST pointers (pinned for full copy/compute overlap; pageable works but
  * serialises).  The library allocates device buffers from a cached pool, copies

@@ -119,6 +119,21 @@ def bound(K: int, alpha: float, beta: float, mag: np.ndarray, C0: np.ndarray | N
     return b
 
 
+U32 = 2.0 ** -23   # fp32 unit roundoff allowing directed (truncating) rounding in the accumulator
+
+
+def bound_f32(K: int, alpha: float, beta: float, mag: np.ndarray, C0: np.ndarray | None) -> np.ndarray:
+    """Elementwise bound for the single-precision (3xTF32) path, reading R16:
+    (4K + 8) u32 |alpha| mag + 4 u32 |beta| |C0| + 1e-30, u32 = 2^-23.
+    4K u32 mag covers the K-term recursive FP32 accumulation of three tf32 product passes
+    with a possibly truncating accumulator; 8 u32 mag covers the 3xTF32 representation
+    error (dropped lo*lo term and the two tf32 roundings, <= 3 * 2^-22 |a||b|)."""
+    b = (4.0 * K + 8.0) * U32 * abs(alpha) * mag + 1e-30
+    if beta != 0.0 and C0 is not None:
+        b = b + 4.0 * U32 * abs(beta) * np.abs(C0)
+    return b
+
+
 @dataclass
 class CheckResult:
     ok: bool

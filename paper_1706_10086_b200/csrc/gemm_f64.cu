@@ -116,6 +116,25 @@ int make_tmap(CUtensorMap *map, const double *ptr, int64_t rows, int64_t cols, i
     return GEMM_OK;
 }
 
+// fp32 row-major rows x cols (ld elements), box = box_cols x box_rows, 128-byte swizzle
+// (box_cols * 4 must be 128).  Used by the 3xTF32 single-precision path (sgemm_tf32.cu).
+int make_tmap_f32(CUtensorMap *map, const float *ptr, int64_t rows, int64_t cols, int64_t ld, int box_cols,
+                  int box_rows) {
+    auto fn = encode_fn();
+    if (!fn) return set_error(GEMM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+    cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1u, 1u};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(ptr), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        return set_error(GEMM_ERR_CUDA, "cuTensorMapEncodeTiled(f32) failed (%d) rows=%lld cols=%lld ld=%lld", (int)r,
+                         (long long)rows, (long long)cols, (long long)ld);
+    return GEMM_OK;
+}
+
 static int encode_tmap(CUtensorMap *map, const double *ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
     auto fn = encode_fn();
     if (!fn) return set_error(GEMM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
@@ -338,9 +357,30 @@ struct SplitWs {
     size_t ws_cap = 0;
     int *ctr = nullptr;
     size_t ctr_cap = 0;
+    double *pack[2] = {nullptr, nullptr};   // repacked A / B (aligned, even leading dimension)
+    size_t pack_cap[2] = {0, 0};
 };
 static std::mutex g_ws_mu;
 static std::map<std::pair<int, cudaStream_t>, SplitWs> g_ws;
+
+// Repack buffer `which` (0 = A, 1 = B) of at least `doubles` elements for stream st.
+static double *get_pack_buf(cudaStream_t st, int which, size_t doubles) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    SplitWs &w = g_ws[{dev, st}];
+    if (w.pack_cap[which] < doubles) {
+        if (w.pack[which]) cudaFree(w.pack[which]);
+        w.pack[which] = nullptr;
+        w.pack_cap[which] = 0;
+        if (cudaMalloc(&w.pack[which], doubles * sizeof(double)) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        w.pack_cap[which] = doubles;
+    }
+    return w.pack[which];
+}
 
 static int get_split_ws(cudaStream_t st, size_t doubles, size_t tiles, double **ws, int **ctr) {
     int dev = 0;
@@ -432,7 +472,40 @@ int gemm_impl(int64_t M, int64_t N, int64_t K, double alpha, const double *A, in
     // TMA stride rule (multiple of 16 bytes) does not exclude it
     if (M == 1) lda += (lda & 1);
     if (K == 1) ldb += (ldb & 1);
-    const bool tma = tma_ok(A, lda, B, ldb);
+    bool tma = tma_ok(A, lda, B, ldb);
+    // Large problems whose operands miss the TMA rules (odd leading dimension, 8-byte-only
+    // alignment) are repacked into aligned workspace rows (2-D copies on the same stream,
+    // O(MK + KN) bytes against O(MNK) flops) and take the TMA path; values and hence the
+    // per-entry arithmetic are unchanged.  Small ones, or if the workspace cannot be had,
+    // run the cp.async kernel.
+    if (!tma && cfg_id < 0 && 2.0 * (double)M * (double)N * (double)K >= 4e9 && M >= 64 && N >= 64 && K >= 16) {
+        const double *pA = A, *pB = B;
+        int64_t plda = lda, pldb = ldb;
+        bool ok = true;
+        if (((uintptr_t)A % 16) || (lda & 1)) {
+            plda = K + (K & 1);
+            double *buf = get_pack_buf(st, 0, (size_t)M * plda);
+            ok = buf && cudaMemcpy2DAsync(buf, plda * 8, A, lda * 8, K * 8, M, cudaMemcpyDeviceToDevice, st) ==
+                            cudaSuccess;
+            pA = buf;
+        }
+        if (ok && (((uintptr_t)B % 16) || (ldb & 1))) {
+            pldb = N + (N & 1);
+            double *buf = get_pack_buf(st, 1, (size_t)K * pldb);
+            ok = buf && cudaMemcpy2DAsync(buf, pldb * 8, B, ldb * 8, N * 8, K, cudaMemcpyDeviceToDevice, st) ==
+                            cudaSuccess;
+            pB = buf;
+        }
+        if (ok && tma_ok(pA, plda, pB, pldb)) {
+            A = pA;
+            B = pB;
+            lda = plda;
+            ldb = pldb;
+            tma = true;
+        } else {
+            cudaGetLastError();
+        }
+    }
     int id = cfg_id;
     int splits = 1;
     if (id < 0) {

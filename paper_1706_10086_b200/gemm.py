@@ -20,7 +20,7 @@ STATUS_NAMES = {0: "GEMM_OK", 1: "GEMM_ERR_ARG", 2: "GEMM_ERR_CUDA", 3: "GEMM_ER
 FILL_MODES = {"uniform": 0, "dyadic": 1, "int8": 2, "ones": 3, "identity": 4, "zeros": 5}
 
 # every symbol include/gemm_f64.h declares (tests check the library exports them all)
-EXPORTS = ("gemm_f64", "gemm_f64_stream", "gemm_f64_cfg", "gemm_f64_ex", "gemm_f64_host", "gemm_host_pool_release",
+EXPORTS = ("gemm_f64", "gemm_f64_stream", "gemm_f64_cfg", "gemm_f64_ex", "gemm_f32", "gemm_f32_stream", "gemm_f64_host", "gemm_host_pool_release",
            "gemm_num_cfgs", "gemm_cfg_name", "gemm_cfg_info", "gemm_cfg_select", "gemm_plan", "gemm_plan_set",
            "gemm_plan_clear", "gemm_tune_load", "gemm_last_error",
            "gemm_fill_f64", "gemm_peak_probe", "gemm_comm_unique_id", "gemm_comm_init",
@@ -50,6 +50,8 @@ def _load():
         "gemm_f64_stream": (ci, core + [vp]),
         "gemm_f64_cfg": (ci, core + [ci, vp]),
         "gemm_f64_ex": (ci, core + [ci, ci, vp]),
+        "gemm_f32": (ci, [i64, i64, i64, ctypes.c_float, vp, i64, vp, i64, ctypes.c_float, vp, i64]),
+        "gemm_f32_stream": (ci, [i64, i64, i64, ctypes.c_float, vp, i64, vp, i64, ctypes.c_float, vp, i64, vp]),
         "gemm_f64_host": (ci, core),
         "gemm_host_pool_release": (ci, []),
         "gemm_num_cfgs": (ci, []),
@@ -98,10 +100,10 @@ def _check(rc: int):
 
 
 # ------------------------------------------------------------------ tensors
-def _mat(x, name):
-    """(ptr, rows, cols, ld) of a 2-D float64 tensor with unit column stride."""
-    if x.dtype.__str__() not in ("torch.float64", "float64"):
-        raise TypeError(f"{name} must be float64, got {x.dtype}")
+def _mat(x, name, dtype="float64"):
+    """(ptr, rows, cols, ld) of a 2-D float64 (or float32) tensor with unit column stride."""
+    if x.dtype.__str__() not in (f"torch.{dtype}", dtype):
+        raise TypeError(f"{name} must be {dtype}, got {x.dtype}")
     if x.dim() != 2:
         raise ValueError(f"{name} must be 2-D")
     r, c = x.shape
@@ -143,6 +145,18 @@ def gemm(A, B, C, alpha: float = 1.0, beta: float = 0.0, cfg: int | None = None,
         rc = _lib.gemm_f64_ex(M, N, K, float(alpha), pa, lda, pb, ldb, float(beta), pc, ldc,
                               -1 if cfg is None else int(cfg), int(splits), st)
     _check(rc)
+    return C
+
+
+def gemm_f32(A, B, C, alpha: float = 1.0, beta: float = 0.0, stream=None):
+    """C <- alpha*A@B + beta*C in single precision on the tensor cores (3xTF32), torch CUDA
+    float32 tensors, row-major.  Returns C."""
+    pa, M, K, lda = _mat(A, "A", "float32")
+    pb, K2, N, ldb = _mat(B, "B", "float32")
+    pc, M2, N2, ldc = _mat(C, "C", "float32")
+    if K2 != K or M2 != M or N2 != N:
+        raise ValueError(f"shape mismatch A{tuple(A.shape)} B{tuple(B.shape)} C{tuple(C.shape)}")
+    _check(_lib.gemm_f32_stream(M, N, K, float(alpha), pa, lda, pb, ldb, float(beta), pc, ldc, _stream_ptr(stream)))
     return C
 
 

@@ -294,3 +294,17 @@ def test_synth_column_block_consistency():
     assert np.array_equal(full[5:17, 20:41], synth.matrix("uniform", 3, 1, 40, 57, row0=5, nrows=12, col0=20, ncols=21))
     eye = synth.matrix("identity", 0, 0, 9, 9)
     assert np.array_equal(eye[2:7, 3:8], synth.matrix("identity", 0, 0, 9, 9, row0=2, nrows=5, col0=3, ncols=5))
+
+
+def test_bound_f32_catches_fp32_scale_errors():
+    """The single-precision bound accepts an FP32 rounding of the fp64 oracle result and a
+    one-ulp(fp32) perturbation, but rejects an error of one dropped k term."""
+    A, B, C0 = synth.problem(32, 32, 512, seed=13)
+    A, B, C0 = (x.astype(np.float32).astype(np.float64) for x in (A, B, C0))
+    C, mag = oracle.dgemm(1.0, A, B, 0.0, C0, want_mag=True)
+    bnd = oracle.bound_f32(512, 1.0, 0.0, mag, None)
+    C32 = C.astype(np.float32).astype(np.float64)
+    assert oracle.check(C32, C, bnd).ok
+    assert oracle.check(np.nextafter(C32.astype(np.float32), np.float32(np.inf)).astype(np.float64), C, bnd).ok
+    dropped = oracle.dgemm(1.0, A[:, :-1], B[:-1], 0.0, C0)
+    assert not oracle.check(dropped, C, bnd).ok
