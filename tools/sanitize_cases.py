@@ -1,4 +1,4 @@
-"""Small shapes through every configuration, for compute-sanitizer (memcheck / racecheck /
+"""Small shapes through every kernel family, for compute-sanitizer (memcheck / racecheck /
 synccheck / initcheck) runs on the GPU box:
 
     compute-sanitizer --tool memcheck python tools/sanitize_cases.py
@@ -9,6 +9,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_1706_10086_b200 import gemm as G  # noqa: E402
@@ -27,11 +28,26 @@ def main():
         G.fill(B, "uniform", 1, 1)
         G.fill(C, "uniform", 1, 2)
         for info in G.cfgs():
-            G.gemm(A, B, C, 1.5, 0.5, cfg=info["id"])
-            n += 1
+            for s in ((1,) if info["split_k"] == 1 else (1, 3)):
+                G.gemm(A, B, C, 1.5, 0.5, cfg=info["id"], splits=s)
+                n += 1
         G.gemm(A, B, C, 0.0, 0.5)            # scale path
+        a32, b32 = A.float(), B.float()
+        c32 = torch.zeros((M, N), dtype=torch.float32, device="cuda")
+        G.gemm_f32(a32, b32, c32, 1.5, 0.5)  # 3xTF32 tcgen05 path
+        n += 2
+    # repack path: large problem with odd leading dimensions
+    M, N, K = 1200, 1201, 1501
+    A = torch.rand((M, K), dtype=torch.float64, device="cuda")
+    B = torch.rand((K, N), dtype=torch.float64, device="cuda")
+    C = torch.zeros((M, N), dtype=torch.float64, device="cuda")
+    G.gemm(A, B, C, 1.0, 0.0)
+    # host entry point
+    hA, hB = np.random.rand(300, 200), np.random.rand(200, 100)
+    hC = np.zeros((300, 100))
+    G.gemm_host(hA, hB, hC, 1.0, 0.0)
     torch.cuda.synchronize()
-    print(f"sanitize cases ok: {n} launches")
+    print(f"sanitize cases ok: {n + 2} calls")
 
 
 if __name__ == "__main__":
