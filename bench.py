@@ -247,7 +247,11 @@ def main():
     if world != a.gpus:
         print(f"warning: --gpus {a.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
     torch.cuda.set_device(local)
-    if world > 1:
+    # launched by torchrun (even with one rank): take the distributed path -- process group,
+    # library NCCL communicator, broadcast of B every step -- so N=1 under torchrun runs
+    # the same code as N>1 (an in-place 1-rank broadcast is a no-op)
+    distributed = world > 1 or "TORCHELASTIC_RUN_ID" in os.environ or "GEMM_BENCH_FORCE_DIST" in os.environ
+    if distributed:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     M, N, K, scaling, wname = workload(a.workload, world)
@@ -263,7 +267,7 @@ def main():
         dB.zero_()
     G.fill(dC, "uniform", 1706, 2, rows=M, row0=r0)
     stream = torch.cuda.current_stream()
-    comm = G.Comm(rank, world) if world > 1 else None
+    comm = G.Comm(rank, world) if distributed else None
     # the product's own plan (heuristic entry point) unless a configuration is forced
     cfg = a.cfg if a.cfg >= 0 else None
     plan_cfg, plan_splits = G.plan(Ml, N, K, dA.data_ptr(), K, dB.data_ptr(), N)
@@ -283,7 +287,7 @@ def main():
     for _ in range(a.warmup):
         step()
     torch.cuda.synchronize()
-    if world > 1:
+    if distributed:
         dist.barrier()
     torch.cuda.synchronize()
 
@@ -304,7 +308,7 @@ def main():
         step(kev[i])
     e_end.record(stream)
     torch.cuda.synchronize()
-    if world > 1:
+    if distributed:
         dist.barrier()
     torch.cuda.synchronize()
     sampler.stop()
@@ -372,7 +376,7 @@ def main():
         print(json.dumps(line), flush=True)
     if comm is not None:
         comm.close()
-    if world > 1:
+    if distributed:
         dist.destroy_process_group()
     return 0
 

@@ -112,6 +112,13 @@ GEMM_API int gemm_f32(int64_t M, int64_t N, int64_t K, float alpha,
 GEMM_API int gemm_f32_stream(int64_t M, int64_t N, int64_t K, float alpha,
                     const float *A, int64_t lda, const float *B, int64_t ldb,
                     float beta, float *C, int64_t ldc, void *cuda_stream);
+/* Same, forcing single-precision tile configuration cfg_id (-1 = default);
+ * gemm_f32_num_cfgs / gemm_f32_cfg_name enumerate them ("tf32x3_128x<BN>x<BK>_s<stages>"). */
+GEMM_API int gemm_f32_cfg(int64_t M, int64_t N, int64_t K, float alpha,
+                 const float *A, int64_t lda, const float *B, int64_t ldb,
+                 float beta, float *C, int64_t ldc, int cfg_id, void *cuda_stream);
+GEMM_API int gemm_f32_num_cfgs(void);
+GEMM_API int gemm_f32_cfg_name(int cfg_id, char *buf, int len);
 
 /* Host-buffer entry point ("the call a user makes" with host data): A, B, C are
  * HOST pointers (pinned for full copy/compute overlap; pageable works but

@@ -116,8 +116,8 @@ int make_tmap(CUtensorMap *map, const double *ptr, int64_t rows, int64_t cols, i
     return GEMM_OK;
 }
 
-// fp32 row-major rows x cols (ld elements), box = box_cols x box_rows, 128-byte swizzle
-// (box_cols * 4 must be 128).  Used by the 3xTF32 single-precision path (sgemm_tf32.cu).
+// fp32 row-major rows x cols (ld elements), box = box_cols x box_rows; the swizzle span equals
+// the box row (32 fp32 -> 128-byte swizzle, 16 -> 64-byte).  Used by the 3xTF32 path (sgemm_tf32.cu).
 int make_tmap_f32(CUtensorMap *map, const float *ptr, int64_t rows, int64_t cols, int64_t ld, int box_cols,
                   int box_rows) {
     auto fn = encode_fn();
@@ -126,8 +126,10 @@ int make_tmap_f32(CUtensorMap *map, const float *ptr, int64_t rows, int64_t cols
     cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
     cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1u, 1u};
+    if (box_cols != 32 && box_cols != 16) return set_error(GEMM_ERR_ARG, "f32 box_cols=%d must be 16 or 32", box_cols);
+    const CUtensorMapSwizzle sw = box_cols == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
     CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(ptr), dims, strides, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS)
         return set_error(GEMM_ERR_CUDA, "cuTensorMapEncodeTiled(f32) failed (%d) rows=%lld cols=%lld ld=%lld", (int)r,

@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <map>
 #include <mutex>
 
@@ -40,15 +41,19 @@ int make_tmap_f32(CUtensorMap *map, const float *ptr, int64_t rows, int64_t cols
 namespace f32 {
 
 constexpr int BM = 128;
-constexpr int BK = 32;   // one 128-byte swizzle row of fp32 along k (A)
 constexpr int UMMA_K = 8;
 
-template <int BN_, int STAGES_>
+// BK = 32 fp32 per k-stage row (128 B, 128-byte swizzle) or 16 (64 B, 64-byte swizzle)
+template <int BN_, int BK_, int STAGES_>
 struct Cfg {
-    static constexpr int BN = BN_, STAGES = STAGES_;
+    static constexpr int BN = BN_, BK = BK_, STAGES = STAGES_;
     static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "UMMA N for M=128: multiple of 16, <= 256");
-    static constexpr uint32_t A_BYTES = BM * BK * 4;            // 16 KB, one of hi / lo
-    static constexpr uint32_t B_BYTES = BN * BK * 4;            // BN rows of B^T x 128 B, one of hi / lo
+    static_assert(BK == 32 || BK == 16, "k-stage row = one 128-byte or 64-byte swizzle row");
+    static constexpr uint32_t ROW_BYTES = BK * 4;                // 128 or 64
+    static constexpr uint32_t SBO = 8 * ROW_BYTES;               // 8-row core-matrix group stride
+    static constexpr uint32_t LAYOUT = BK == 32 ? 2u : 4u;       // UMMA SWIZZLE_128B / SWIZZLE_64B
+    static constexpr uint32_t A_BYTES = BM * BK * 4;            // one of hi / lo
+    static constexpr uint32_t B_BYTES = BN * BK * 4;            // BN rows of B^T, one of hi / lo
     static constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
     // two FP32 accumulators of BN columns each: hi*hi and the lo correction terms
     static constexpr uint32_t TMEM_COLS = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 :
@@ -61,13 +66,13 @@ struct Cfg {
 // Shared-memory matrix descriptor (sm_100 UMMA): start>>4 [0,14), LBO>>4 [16,30),
 // SBO>>4 [32,46), version 1 [46,48), base offset [49,52), layout type [61,64)
 // (2 = 128-byte swizzle).
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout = 2) {
     uint64_t d = 0;
     d |= (uint64_t)((saddr >> 4) & 0x3FFF);
     d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
     d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
     d |= (uint64_t)1 << 46;
-    d |= (uint64_t)2 << 61;
+    d |= (uint64_t)layout << 61;
     return d;
 }
 
@@ -138,6 +143,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     tile_coords(blockIdx.x, tiles_m, tiles_n, group_m, tm, tn);
     const int m0 = tm * BM, n0 = tn * C::BN;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int BK = C::BK;
     const int KT = (K + BK - 1) / BK;
 
     if (threadIdx.x == 0) {
@@ -194,16 +200,16 @@ __global__ void __launch_bounds__(C::THREADS, 1)
                 for (int kk = 0; kk < BK / UMMA_K; ++kk) {
                     // K-major, rows of 128 B (32 k), 8-row groups 1024 B apart (SBO); the
                     // 8-deep k-step advances the start address by 32 B inside the swizzle atom
-                    const uint64_t a_hi = umma_desc(sa + kk * 32, 0, 1024);
-                    const uint64_t b_hi = umma_desc(sb + kk * 32, 0, 1024);
+                    const uint64_t a_hi = umma_desc(sa + kk * 32, 0, C::SBO, C::LAYOUT);
+                    const uint64_t b_hi = umma_desc(sb + kk * 32, 0, C::SBO, C::LAYOUT);
                     umma_tf32(tmem, a_hi, b_hi, idesc, (kt > 0 || kk > 0) ? 1u : 0u);
                 }
 #pragma unroll
                 for (int kk = 0; kk < BK / UMMA_K; ++kk) {
-                    const uint64_t a_hi = umma_desc(sa + kk * 32, 0, 1024);
-                    const uint64_t a_lo = umma_desc(sa + C::A_BYTES + kk * 32, 0, 1024);
-                    const uint64_t b_hi = umma_desc(sb + kk * 32, 0, 1024);
-                    const uint64_t b_lo = umma_desc(sb + C::B_BYTES + kk * 32, 0, 1024);
+                    const uint64_t a_hi = umma_desc(sa + kk * 32, 0, C::SBO, C::LAYOUT);
+                    const uint64_t a_lo = umma_desc(sa + C::A_BYTES + kk * 32, 0, C::SBO, C::LAYOUT);
+                    const uint64_t b_hi = umma_desc(sb + kk * 32, 0, C::SBO, C::LAYOUT);
+                    const uint64_t b_lo = umma_desc(sb + C::B_BYTES + kk * 32, 0, C::SBO, C::LAYOUT);
                     umma_tf32(tmem + C::BN, a_lo, b_hi, idesc, (kt > 0 || kk > 0) ? 1u : 0u);
                     umma_tf32(tmem + C::BN, a_hi, b_lo, idesc, 1u);
                 }
@@ -304,7 +310,36 @@ __global__ void scale_f32_kernel(int M, int N, float beta, float *__restrict__ C
     }
 }
 
-using DefaultCfg = Cfg<128, 3>;
+struct F32Cfg {
+    const char *name;
+    int bn, bk, stages;
+    uint32_t smem;
+    const void *kernel;
+    void (*launch)(dim3, cudaStream_t, const CUtensorMap &, const CUtensorMap &, const CUtensorMap &,
+                   const CUtensorMap &, int, int, int, float, float, float *, int64_t, int);
+};
+
+template <class C>
+static void launch_f32(dim3 grid, cudaStream_t st, const CUtensorMap &a, const CUtensorMap &b, const CUtensorMap &c,
+                       const CUtensorMap &d, int M, int N, int K, float alpha, float beta, float *Cm, int64_t ldc,
+                       int group_m) {
+    sgemm_3xtf32_kernel<C><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(a, b, c, d, M, N, K, alpha, beta, Cm, ldc,
+                                                                     group_m);
+}
+
+#define F32CFG(BN, BK, ST)                                                                                   \
+    F32Cfg{"tf32x3_128x" #BN "x" #BK "_s" #ST, BN, BK, ST, Cfg<BN, BK, ST>::SMEM_BYTES,                       \
+           (const void *)sgemm_3xtf32_kernel<Cfg<BN, BK, ST>>, launch_f32<Cfg<BN, BK, ST>>}
+
+static const F32Cfg k_f32_cfgs[] = {
+    F32CFG(128, 32, 3),
+    F32CFG(128, 16, 6),
+    F32CFG(256, 32, 2),
+    F32CFG(256, 16, 4),
+};
+static constexpr int kNumF32Cfgs = sizeof(k_f32_cfgs) / sizeof(k_f32_cfgs[0]);
+static constexpr int kDefaultF32 = 0;   // tf32x3_128x128x32_s3
+static constexpr int kWideF32 = 3;      // tf32x3_128x256x16_s4 (measured best at 8192 / 16384)
 
 struct Ws {
     float *buf = nullptr;
@@ -312,7 +347,7 @@ struct Ws {
 };
 static std::mutex g_mu;
 static std::map<std::pair<int, cudaStream_t>, Ws> g_ws;
-static std::map<int, bool> g_attr;
+static std::map<int, bool> g_attr;   // (device * 64 + cfg) -> smem attribute set
 
 static float *workspace(cudaStream_t st, size_t floats) {
     int dev = 0;
@@ -341,7 +376,7 @@ static bool overlaps(const void *p, int64_t rows, int64_t cols, int64_t ld, cons
 }
 
 static int impl(int64_t M, int64_t N, int64_t K, float alpha, const float *A, int64_t lda, const float *B,
-                int64_t ldb, float beta, float *C, int64_t ldc, cudaStream_t st) {
+                int64_t ldb, float beta, float *C, int64_t ldc, cudaStream_t st, int cfg_id = -1) {
     clear_error();
     if (M < 0 || N < 0 || K < 0)
         return set_error(GEMM_ERR_ARG, "M=%lld N=%lld K=%lld must be >= 0", (long long)M, (long long)N, (long long)K);
@@ -368,7 +403,10 @@ static int impl(int64_t M, int64_t N, int64_t K, float alpha, const float *A, in
         scale_f32_kernel<<<blocks, 256, 0, st>>>((int)M, (int)N, beta, C, ldc);
         return cuda_check(cudaGetLastError(), "scale_f32_kernel launch");
     }
-    using Cf = DefaultCfg;
+    if (cfg_id < -1 || cfg_id >= kNumF32Cfgs)
+        return set_error(GEMM_ERR_ARG, "f32 cfg_id=%d out of range [-1, %d)", cfg_id, kNumF32Cfgs);
+    // default: 128 x 256 tiles (fewer L2 bytes per FLOP) unless N is small
+    const F32Cfg &cf = k_f32_cfgs[cfg_id >= 0 ? cfg_id : (N > 128 ? kWideF32 : kDefaultF32)];
     // split A and B into tf32 hi / lo in workspace, row pitch padded to 16 bytes
     const int64_t ka = (K + 3) & ~int64_t(3);
     const size_t a_sz = (size_t)M * ka, b_sz = (size_t)N * ka;   // A and B^T, both K-major
@@ -385,26 +423,25 @@ static int impl(int64_t M, int64_t N, int64_t K, float alpha, const float *A, in
         if (rc) return rc;
     }
     CUtensorMap mAh, mAl, mBh, mBl;
-    int rc = make_tmap_f32(&mAh, Ah, M, K, ka, 32, BM);
-    if (!rc) rc = make_tmap_f32(&mAl, Al, M, K, ka, 32, BM);
-    if (!rc) rc = make_tmap_f32(&mBh, Bh, N, K, ka, 32, Cf::BN);
-    if (!rc) rc = make_tmap_f32(&mBl, Bl, N, K, ka, 32, Cf::BN);
+    int rc = make_tmap_f32(&mAh, Ah, M, K, ka, cf.bk, BM);
+    if (!rc) rc = make_tmap_f32(&mAl, Al, M, K, ka, cf.bk, BM);
+    if (!rc) rc = make_tmap_f32(&mBh, Bh, N, K, ka, cf.bk, cf.bn);
+    if (!rc) rc = make_tmap_f32(&mBl, Bl, N, K, ka, cf.bk, cf.bn);
     if (rc) return rc;
     int dev = 0;
     cudaGetDevice(&dev);
     {
         std::lock_guard<std::mutex> lk(g_mu);
-        if (!g_attr[dev]) {
-            rc = cuda_check(cudaFuncSetAttribute(sgemm_3xtf32_kernel<Cf>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 Cf::SMEM_BYTES),
+        const int key = dev * 64 + (int)(&cf - k_f32_cfgs);
+        if (!g_attr[key]) {
+            rc = cuda_check(cudaFuncSetAttribute(cf.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, cf.smem),
                             "cudaFuncSetAttribute(sgemm)");
             if (rc) return rc;
-            g_attr[dev] = true;
+            g_attr[key] = true;
         }
     }
-    const int tiles = (int)(((M + BM - 1) / BM) * ((N + Cf::BN - 1) / Cf::BN));
-    sgemm_3xtf32_kernel<Cf><<<tiles, Cf::THREADS, Cf::SMEM_BYTES, st>>>(mAh, mAl, mBh, mBl, (int)M, (int)N, (int)K,
-                                                                        alpha, beta, C, ldc, 8);
+    const int tiles = (int)(((M + BM - 1) / BM) * ((N + cf.bn - 1) / cf.bn));
+    cf.launch(dim3(tiles), st, mAh, mAl, mBh, mBl, (int)M, (int)N, (int)K, alpha, beta, C, ldc, 8);
     return cuda_check(cudaGetLastError(), "sgemm_3xtf32_kernel launch");
 }
 
@@ -421,6 +458,21 @@ int gemm_f32(int64_t M, int64_t N, int64_t K, float alpha, const float *A, int64
 int gemm_f32_stream(int64_t M, int64_t N, int64_t K, float alpha, const float *A, int64_t lda, const float *B,
                     int64_t ldb, float beta, float *C, int64_t ldc, void *stream) {
     return dg::f32::impl(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, (cudaStream_t)stream);
+}
+
+int gemm_f32_cfg(int64_t M, int64_t N, int64_t K, float alpha, const float *A, int64_t lda, const float *B,
+                 int64_t ldb, float beta, float *C, int64_t ldc, int cfg_id, void *stream) {
+    return dg::f32::impl(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, (cudaStream_t)stream, cfg_id);
+}
+
+int gemm_f32_num_cfgs(void) { return dg::f32::kNumF32Cfgs; }
+
+int gemm_f32_cfg_name(int cfg_id, char *buf, int len) {
+    dg::clear_error();
+    if (cfg_id < 0 || cfg_id >= dg::f32::kNumF32Cfgs) return dg::set_error(GEMM_ERR_ARG, "f32 cfg_id out of range");
+    if (!buf || len <= 0) return dg::set_error(GEMM_ERR_ARG, "buf is NULL or len <= 0");
+    snprintf(buf, (size_t)len, "%s", dg::f32::k_f32_cfgs[cfg_id].name);
+    return GEMM_OK;
 }
 
 }  // extern "C"

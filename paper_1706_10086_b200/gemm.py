@@ -20,7 +20,8 @@ STATUS_NAMES = {0: "GEMM_OK", 1: "GEMM_ERR_ARG", 2: "GEMM_ERR_CUDA", 3: "GEMM_ER
 FILL_MODES = {"uniform": 0, "dyadic": 1, "int8": 2, "ones": 3, "identity": 4, "zeros": 5}
 
 # every symbol include/gemm_f64.h declares (tests check the library exports them all)
-EXPORTS = ("gemm_f64", "gemm_f64_stream", "gemm_f64_cfg", "gemm_f64_ex", "gemm_f32", "gemm_f32_stream", "gemm_f64_host", "gemm_host_pool_release",
+EXPORTS = ("gemm_f64", "gemm_f64_stream", "gemm_f64_cfg", "gemm_f64_ex", "gemm_f32", "gemm_f32_stream",
+           "gemm_f32_cfg", "gemm_f32_num_cfgs", "gemm_f32_cfg_name", "gemm_f64_host", "gemm_host_pool_release",
            "gemm_num_cfgs", "gemm_cfg_name", "gemm_cfg_info", "gemm_cfg_select", "gemm_plan", "gemm_plan_set",
            "gemm_plan_clear", "gemm_tune_load", "gemm_last_error",
            "gemm_fill_f64", "gemm_peak_probe", "gemm_comm_unique_id", "gemm_comm_init",
@@ -52,6 +53,9 @@ def _load():
         "gemm_f64_ex": (ci, core + [ci, ci, vp]),
         "gemm_f32": (ci, [i64, i64, i64, ctypes.c_float, vp, i64, vp, i64, ctypes.c_float, vp, i64]),
         "gemm_f32_stream": (ci, [i64, i64, i64, ctypes.c_float, vp, i64, vp, i64, ctypes.c_float, vp, i64, vp]),
+        "gemm_f32_cfg": (ci, [i64, i64, i64, ctypes.c_float, vp, i64, vp, i64, ctypes.c_float, vp, i64, ci, vp]),
+        "gemm_f32_num_cfgs": (ci, []),
+        "gemm_f32_cfg_name": (ci, [ci, ctypes.c_char_p, ci]),
         "gemm_f64_host": (ci, core),
         "gemm_host_pool_release": (ci, []),
         "gemm_num_cfgs": (ci, []),
@@ -148,7 +152,7 @@ def gemm(A, B, C, alpha: float = 1.0, beta: float = 0.0, cfg: int | None = None,
     return C
 
 
-def gemm_f32(A, B, C, alpha: float = 1.0, beta: float = 0.0, stream=None):
+def gemm_f32(A, B, C, alpha: float = 1.0, beta: float = 0.0, stream=None, cfg: int | None = None):
     """C <- alpha*A@B + beta*C in single precision on the tensor cores (3xTF32), torch CUDA
     float32 tensors, row-major.  Returns C."""
     pa, M, K, lda = _mat(A, "A", "float32")
@@ -156,8 +160,22 @@ def gemm_f32(A, B, C, alpha: float = 1.0, beta: float = 0.0, stream=None):
     pc, M2, N2, ldc = _mat(C, "C", "float32")
     if K2 != K or M2 != M or N2 != N:
         raise ValueError(f"shape mismatch A{tuple(A.shape)} B{tuple(B.shape)} C{tuple(C.shape)}")
-    _check(_lib.gemm_f32_stream(M, N, K, float(alpha), pa, lda, pb, ldb, float(beta), pc, ldc, _stream_ptr(stream)))
+    if cfg is None:
+        _check(_lib.gemm_f32_stream(M, N, K, float(alpha), pa, lda, pb, ldb, float(beta), pc, ldc,
+                                    _stream_ptr(stream)))
+    else:
+        _check(_lib.gemm_f32_cfg(M, N, K, float(alpha), pa, lda, pb, ldb, float(beta), pc, ldc, int(cfg),
+                                 _stream_ptr(stream)))
     return C
+
+
+def f32_cfg_names() -> list:
+    out = []
+    for i in range(_lib.gemm_f32_num_cfgs()):
+        buf = ctypes.create_string_buffer(64)
+        _check(_lib.gemm_f32_cfg_name(i, buf, 64))
+        out.append(buf.value.decode())
+    return out
 
 
 def gemm_raw(M, N, K, alpha, A_ptr, lda, B_ptr, ldb, beta, C_ptr, ldc, cfg=-1, stream=0) -> int:

@@ -105,3 +105,17 @@ def test_f32_large_sampled_rows(cuda_lib):
     got = c32[torch.tensor(rows, device="cuda")].cpu().numpy().astype(np.float64)
     r = oracle.check(got, ref, oracle.bound_f32(K, 1.0, 0.0, mag, None))
     assert r.ok, str(r)
+
+
+@pytest.mark.parametrize("shape", [(130, 300, 77), (256, 512, 1000), (1, 1, 1)], ids=lambda s: "x".join(map(str, s)))
+def test_f32_every_cfg_within_bound(cuda_lib, shape):
+    M, N, K = shape
+    A, B, C0 = (f32(x).astype(np.float64) for x in synth.problem(M, N, K, seed=M + K))
+    ref, mag = oracle.dgemm(1.5, A, B, 0.5, C0, want_mag=True)
+    bnd = oracle.bound_f32(K, 1.5, 0.5, mag, C0)
+    for cfg in range(len(cuda_lib.f32_cfg_names())):
+        dA, dB, dC = (torch.from_numpy(f32(x)).cuda() for x in (A, B, C0))
+        cuda_lib.gemm_f32(dA, dB, dC, 1.5, 0.5, cfg=cfg)
+        torch.cuda.synchronize()
+        r = oracle.check(dC.cpu().numpy().astype(np.float64), ref, bnd)
+        assert r.ok, (cuda_lib.f32_cfg_names()[cfg], str(r))

@@ -25,26 +25,29 @@ def main():
     ap.add_argument("--sizes", default="4096,8192,16384")
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--out", default="gpurun_out/f32.json")
+    ap.add_argument("--cfgs", default="default", help="'default', 'all' or comma list of f32 cfg ids")
     a = ap.parse_args()
     res = []
-    for n in (int(x) for x in a.sizes.split(",")):
+    cfgs = [None] if a.cfgs == "default" else (list(range(len(G.f32_cfg_names()))) if a.cfgs == "all"
+                                                  else [int(x) for x in a.cfgs.split(",")])
+    for n, cfg in ((int(x), c) for x in a.sizes.split(",") for c in cfgs):
         A = torch.rand((n, n), dtype=torch.float32, device="cuda") * 2 - 1
         B = torch.rand((n, n), dtype=torch.float32, device="cuda") * 2 - 1
         C = torch.zeros((n, n), dtype=torch.float32, device="cuda")
         t0 = time.time()
         while time.time() - t0 < 0.3:
-            G.gemm_f32(A, B, C, 1.0, 0.0)
+            G.gemm_f32(A, B, C, 1.0, 0.0, cfg=cfg)
             torch.cuda.synchronize()
         ts = []
         for _ in range(a.reps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            G.gemm_f32(A, B, C, 1.0, 0.0)
+            G.gemm_f32(A, B, C, 1.0, 0.0, cfg=cfg)
             e1.record()
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1) * 1e-3)
         fl = 2.0 * n ** 3
-        r = {"n": n, "best_s": min(ts), "median_s": statistics.median(ts), "tflops": fl / min(ts) / 1e12,
+        r = {"n": n, "cfg": G.f32_cfg_names()[cfg] if cfg is not None else "default", "best_s": min(ts), "median_s": statistics.median(ts), "tflops": fl / min(ts) / 1e12,
              "roof_tf32_over_3": 1100.0 / 3, "roof_fp32_simt": 148 * 128 * 2 * 1.965e9 / 1e12}
         print(json.dumps(r), flush=True)
         res.append(r)
