@@ -40,7 +40,7 @@
  * - Argument rules: M, N, K >= 0; lda >= max(1, K); ldb >= max(1, N);
  *   ldc >= max(1, N); A, B non-NULL when alpha != 0 and K > 0 and M*N > 0;
  *   C non-NULL when M*N > 0; all pointers 8-byte aligned; C must not overlap
- *   A or B.  M, N, K < 2^31.
+ *   A or B.  M, N, K < 2^31 - 4096 (32-bit tile arithmetic / TMA coordinates).
  *   Pointers 16-byte aligned with even lda/ldb take the TMA path; anything
  *   else takes a slower GPU path (cp.async staging).  There is no CPU path.
  */

@@ -430,9 +430,9 @@ int validate(int64_t M, int64_t N, int64_t K, double alpha, const double *A, int
     if (M < 0) return set_error(GEMM_ERR_ARG, "M=%lld must be >= 0", (long long)M);
     if (N < 0) return set_error(GEMM_ERR_ARG, "N=%lld must be >= 0", (long long)N);
     if (K < 0) return set_error(GEMM_ERR_ARG, "K=%lld must be >= 0", (long long)K);
-    const int64_t lim = (int64_t(1) << 31) - 1;
+    const int64_t lim = (int64_t(1) << 31) - 4096;   // int32 tile arithmetic and TMA coordinates
     if (M > lim || N > lim || K > lim)
-        return set_error(GEMM_ERR_UNSUPPORTED, "M, N, K must be < 2^31 (M=%lld N=%lld K=%lld)", (long long)M,
+        return set_error(GEMM_ERR_UNSUPPORTED, "M, N, K must be < 2^31 - 4096 (M=%lld N=%lld K=%lld)", (long long)M,
                          (long long)N, (long long)K);
     if (lda < std::max<int64_t>(1, K))
         return set_error(GEMM_ERR_ARG, "lda=%lld must be >= max(1,K=%lld)", (long long)lda, (long long)K);

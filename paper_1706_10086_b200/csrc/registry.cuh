@@ -39,8 +39,9 @@ static int launch_tma(const LaunchArgs &a, cudaStream_t st) {
     if (rc) return rc;
     rc = make_tmap(&tb, a.B, a.K, a.N, a.ldb, 16);
     if (rc) return rc;
-    const int tiles = ((a.M + C::BM - 1) / C::BM) * ((a.N + C::BN - 1) / C::BN);
-    dim3 grid(tiles, SPLIT ? a.sk.splits : 1);
+    const int64_t tiles = ((int64_t)a.M + C::BM - 1) / C::BM * (((int64_t)a.N + C::BN - 1) / C::BN);
+    if (tiles > 0x7FFFFFFF) return set_error(GEMM_ERR_UNSUPPORTED, "too many tiles (%lld)", (long long)tiles);
+    dim3 grid((unsigned)tiles, SPLIT ? a.sk.splits : 1);
     dgemm_tma_kernel<C, SPLIT, XP><<<grid, C::CONSUMER_THREADS, C::SMEM_BYTES, st>>>(
         ta, tb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec, a.group_m, a.sk);
     return cuda_check(cudaGetLastError(), "dgemm_tma_kernel launch");
@@ -48,8 +49,9 @@ static int launch_tma(const LaunchArgs &a, cudaStream_t st) {
 
 template <class C>
 static int launch_generic(const LaunchArgs &a, cudaStream_t st) {
-    const int tiles = ((a.M + C::BM - 1) / C::BM) * ((a.N + C::BN - 1) / C::BN);
-    dgemm_generic_kernel<C><<<tiles, C::CONSUMER_THREADS, C::SMEM_BYTES, st>>>(
+    const int64_t tiles = ((int64_t)a.M + C::BM - 1) / C::BM * (((int64_t)a.N + C::BN - 1) / C::BN);
+    if (tiles > 0x7FFFFFFF) return set_error(GEMM_ERR_UNSUPPORTED, "too many tiles (%lld)", (long long)tiles);
+    dgemm_generic_kernel<C><<<(unsigned)tiles, C::CONSUMER_THREADS, C::SMEM_BYTES, st>>>(
         a.A, a.lda, a.B, a.ldb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec, a.group_m);
     return cuda_check(cudaGetLastError(), "dgemm_generic_kernel launch");
 }

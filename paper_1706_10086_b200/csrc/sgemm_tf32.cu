@@ -380,7 +380,7 @@ static int impl(int64_t M, int64_t N, int64_t K, float alpha, const float *A, in
     clear_error();
     if (M < 0 || N < 0 || K < 0)
         return set_error(GEMM_ERR_ARG, "M=%lld N=%lld K=%lld must be >= 0", (long long)M, (long long)N, (long long)K);
-    const int64_t lim = (int64_t(1) << 31) - 1;
+    const int64_t lim = (int64_t(1) << 31) - 4096;   // int32 tile arithmetic and TMA coordinates
     if (M > lim || N > lim || K > lim) return set_error(GEMM_ERR_UNSUPPORTED, "M, N, K must be < 2^31");
     if (lda < std::max<int64_t>(1, K)) return set_error(GEMM_ERR_ARG, "lda=%lld must be >= max(1,K)", (long long)lda);
     if (ldb < std::max<int64_t>(1, N)) return set_error(GEMM_ERR_ARG, "ldb=%lld must be >= max(1,N)", (long long)ldb);
@@ -440,8 +440,9 @@ static int impl(int64_t M, int64_t N, int64_t K, float alpha, const float *A, in
             g_attr[key] = true;
         }
     }
-    const int tiles = (int)(((M + BM - 1) / BM) * ((N + cf.bn - 1) / cf.bn));
-    cf.launch(dim3(tiles), st, mAh, mAl, mBh, mBl, (int)M, (int)N, (int)K, alpha, beta, C, ldc, 8);
+    const int64_t tiles = ((M + BM - 1) / BM) * ((N + cf.bn - 1) / cf.bn);
+    if (tiles > 0x7FFFFFFF) return set_error(GEMM_ERR_UNSUPPORTED, "too many tiles (%lld)", (long long)tiles);
+    cf.launch(dim3((unsigned)tiles), st, mAh, mAl, mBh, mBl, (int)M, (int)N, (int)K, alpha, beta, C, ldc, 8);
     return cuda_check(cudaGetLastError(), "sgemm_3xtf32_kernel launch");
 }
 

@@ -134,6 +134,7 @@ def test_heuristic_selection(G):
     ((4, 4, 4, 1.0, 1024, 4, 4096, 4, 0.0, 1040, 4), "C overlaps A"),
     ((4, 4, 4, 1.0, 1024, 4, 4096, 4, 0.0, 4100 - 4, 4), "C overlaps B"),
     ((2 ** 31, 4, 4, 1.0, 16, 4, 16, 4, 0.0, 16, 4), "< 2^31"),
+    ((2 ** 31 - 100, 4, 4, 1.0, 16, 4, 16, 4, 0.0, 16, 4), "< 2^31"),
 ])
 def test_argument_validation_messages(G, args, needle):
     rc = G.gemm_raw(*args)
@@ -179,3 +180,16 @@ def test_row_range_partition(G):
 def test_unique_id_is_128_bytes_and_fresh(G):
     a, b = G.unique_id(), G.unique_id()
     assert len(a) == 128 and len(b) == 128 and a != b
+
+
+def test_sass_f32_kernels_use_tcgen05(sass):
+    """The single-precision path is Blackwell-native: tcgen05.mma (UTCHMMA), TMEM loads
+    (LDTM), TMA (UTMALDG), no local-memory spills."""
+    funcs = _functions(sass)
+    f32 = {k: v for k, v in funcs.items() if "sgemm_3xtf32" in k}
+    assert len(f32) >= 2
+    for name, body in f32.items():
+        assert "UTCHMMA" in body, name
+        assert "LDTM" in body, name
+        assert "UTMALDG" in body, name
+        assert not re.search(r"\b(LDL|STL)\b", body), name
