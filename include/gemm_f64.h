@@ -142,7 +142,8 @@ typedef struct {
     int threads;        /* threads per CTA (lane 0 of warp 0 doubles as TMA producer) */
     int smem_bytes;     /* dynamic shared memory per CTA                           */
     int tma;            /* 1: TMA + mbarrier pipeline; 0: cp.async staging          */
-    int split_k;        /* 1: no split-K; 0: deterministic split-K, slices chosen per call */
+    int split_k;        /* 1: no split-K; 0: deterministic split-K, slices chosen per call;
+                           -1: stream-K (persistent grid, even k-step share per CTA)   */
     int regs;           /* registers per thread (from cudaFuncGetAttributes; 0 before first use) */
 } gemm_cfg_desc;
 
@@ -163,7 +164,7 @@ GEMM_API int gemm_plan(int64_t M, int64_t N, int64_t K, const double *A, int64_t
 
 /* Auto-tuner hooks (the paper's per-architecture tuning, §2.3, as a
  * persisted per-shape table).  gemm_plan_set pins the plan the heuristic entry
- * points use for (M, N, K, TMA-eligible) on the current device; gemm_plan_clear
+ * points use for (M, N, K, TMA-eligible) on every device; gemm_plan_clear
  * forgets all pinned and cached plans; gemm_tune_load reads a text table with
  * lines "M N K tma cfg_name splits" ('#' comments), pinning each, and writes the
  * number of entries loaded to *n_loaded (may be NULL). */

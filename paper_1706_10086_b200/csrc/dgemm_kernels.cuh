@@ -250,19 +250,22 @@ struct SplitArgs {
 };
 
 template <class C>
-__device__ __forceinline__ double *split_slot(const SplitArgs &sk, int tile, int s, int warp, int lane) {
+__device__ __forceinline__ double *partial_slot(double *ws, int64_t slot, int warp, int lane) {
     constexpr int Q = C::E / 4;   // 256-bit groups per thread
-    return sk.ws + (((int64_t)tile * sk.splits + s) * Q * C::CONSUMER_WARPS * 32 + (int64_t)warp * 32 + lane) * 4;
+    return ws + (slot * Q * C::CONSUMER_WARPS * 32 + (int64_t)warp * 32 + lane) * 4;
 }
 
-// returns true if this CTA must run the epilogue (no split, or last split to arrive)
+// Deterministic reduction of the nseg partial sums of one tile (split-K slices or
+// stream-K segments).  Partial `seg` goes to workspace slot (tile * stride + seg); the
+// CTA arriving last on the tile's counter adds the nseg partials in segment order (so the
+// result is independent of arrival order), resets the counter and returns true with the
+// total in acc; the others return false.
 template <class C>
-__device__ __forceinline__ bool split_reduce(double (&acc)[C::MB][C::NP][2][2], const SplitArgs &sk, int tile,
-                                             int s, int warp, int lane) {
-    if (sk.splits <= 1) return true;
+__device__ __forceinline__ bool partial_reduce(double (&acc)[C::MB][C::NP][2][2], double *ws, int *counters,
+                                               int64_t tile, int stride, int seg, int nseg, int warp, int lane) {
     constexpr int Q = C::E / 4;
     constexpr int64_t QSTRIDE = (int64_t)C::CONSUMER_WARPS * 32 * 4;   // doubles between q groups
-    double *mine = split_slot<C>(sk, tile, s, warp, lane);
+    double *mine = partial_slot<C>(ws, tile * stride + seg, warp, lane);
     double *flat = &acc[0][0][0][0];
 #pragma unroll
     for (int q = 0; q < Q; ++q) stg_v4(mine + q * QSTRIDE, flat[4 * q], flat[4 * q + 1], flat[4 * q + 2], flat[4 * q + 3]);
@@ -270,16 +273,16 @@ __device__ __forceinline__ bool split_reduce(double (&acc)[C::MB][C::NP][2][2], 
     __syncthreads();
     __shared__ int s_last;
     if (threadIdx.x == 0) {
-        const int old = atomicAdd(&sk.counters[tile], 1);
-        s_last = (old == sk.splits - 1);
+        const int old = atomicAdd(&counters[tile], 1);
+        s_last = (old == nseg - 1);
     }
     __syncthreads();
     if (!s_last) return false;
     __threadfence();
 #pragma unroll
     for (int e = 0; e < C::E; ++e) flat[e] = 0.0;
-    for (int t = 0; t < sk.splits; ++t) {
-        const double *src = split_slot<C>(sk, tile, t, warp, lane);
+    for (int t = 0; t < nseg; ++t) {
+        const double *src = partial_slot<C>(ws, tile * stride + t, warp, lane);
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
             double v0, v1, v2, v3;
@@ -292,8 +295,16 @@ __device__ __forceinline__ bool split_reduce(double (&acc)[C::MB][C::NP][2][2], 
             flat[4 * q + 3] += v3;
         }
     }
-    if (threadIdx.x == 0) sk.counters[tile] = 0;
+    if (threadIdx.x == 0) counters[tile] = 0;
     return true;
+}
+
+// returns true if this CTA must run the epilogue (no split, or last split to arrive)
+template <class C>
+__device__ __forceinline__ bool split_reduce(double (&acc)[C::MB][C::NP][2][2], const SplitArgs &sk, int tile,
+                                             int s, int warp, int lane) {
+    if (sk.splits <= 1) return true;
+    return partial_reduce<C>(acc, sk.ws, sk.counters, tile, sk.splits, s, sk.splits, warp, lane);
 }
 
 // SPLIT = false instantiations carry no split-K code (the reduction's registers would
@@ -408,6 +419,167 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
         if (!split_reduce<C>(acc, sk, blockIdx.x, split, warp, lane)) return;
     }
     epilogue<C>(acc, m0 + warp_m * C::WM, n0 + warp_n * C::WN, lane, M, N, alpha, beta, Cm, ldc, vec != 0);
+}
+
+// ------------------------------------------------------------------------------
+// Stream-K kernel (row a5): a persistent grid of G CTAs (SMs x resident CTAs per SM)
+// shares the U = tiles x KT k-steps evenly: CTA g runs global k-steps [g*U/G, (g+1)*U/G),
+// crossing tile boundaries, so no SM idles in a partial last wave.  A tile covered by
+// one CTA gets the plain epilogue; a tile cut by CTA boundaries is finished by
+// partial_reduce (deterministic segment order).  The TMA producer streams k-steps in
+// global order, so the smem ring stays full across tile boundaries.
+__device__ __forceinline__ int64_t sk_bound(int64_t g, int64_t U, int64_t G) { return g * U / G; }
+// number of g in [0, G] with floor(g*U/G) <= x
+__device__ __forceinline__ int64_t sk_count_le(int64_t x, int64_t U, int64_t G) {
+    const int64_t c = ((x + 1) * G + U - 1) / U;   // ceil((x+1) G / U)
+    return c > G + 1 ? G + 1 : c;
+}
+
+template <class C>
+__device__ __forceinline__ bool streamk_reduce(double (&acc)[C::MB][C::NP][2][2], double *ws, int *counters,
+                                               int64_t tile, int64_t my_slot, int64_t t0, int64_t before, int nseg,
+                                               int64_t U, int64_t G, int warp, int lane) {
+    constexpr int Q = C::E / 4;
+    constexpr int64_t QSTRIDE = (int64_t)C::CONSUMER_WARPS * 32 * 4;
+    double *mine = partial_slot<C>(ws, my_slot, warp, lane);
+    double *flat = &acc[0][0][0][0];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) stg_v4(mine + q * QSTRIDE, flat[4 * q], flat[4 * q + 1], flat[4 * q + 2], flat[4 * q + 3]);
+    __threadfence();
+    __syncthreads();
+    __shared__ int s_last_sk;
+    if (threadIdx.x == 0) s_last_sk = (atomicAdd(&counters[tile], 1) == nseg - 1);
+    __syncthreads();
+    if (!s_last_sk) return false;
+    __threadfence();
+#pragma unroll
+    for (int e = 0; e < C::E; ++e) flat[e] = 0.0;
+    for (int j = 0; j < nseg; ++j) {           // segment order = k order
+        const int64_t gj = before - 1 + j;
+        const int64_t slot = 2 * gj + (sk_bound(gj, U, G) >= t0 ? 0 : 1);
+        const double *src = partial_slot<C>(ws, slot, warp, lane);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            double v0, v1, v2, v3;
+            asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];\n"
+                         : "=d"(v0), "=d"(v1), "=d"(v2), "=d"(v3)
+                         : "l"(src + q * QSTRIDE));
+            flat[4 * q] += v0;
+            flat[4 * q + 1] += v1;
+            flat[4 * q + 2] += v2;
+            flat[4 * q + 3] += v3;
+        }
+    }
+    if (threadIdx.x == 0) counters[tile] = 0;
+    return true;
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
+    dgemm_streamk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
+                         int N, int K, double alpha, double beta, double *__restrict__ Cm, int64_t ldc, int vec,
+                         int group_m, double *ws, int *counters) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t *base_ptr = smem_raw + (base - raw);
+    uint64_t *full = reinterpret_cast<uint64_t *>(base_ptr + C::STAGES * C::STAGE_BYTES);
+    uint64_t *empty = full + C::STAGES;
+
+    const int tiles_m = (M + C::BM - 1) / C::BM, tiles_n = (N + C::BN - 1) / C::BN;
+    const int64_t KT = (K + C::BK - 1) / C::BK;
+    const int64_t U = (int64_t)tiles_m * tiles_n * KT, G = gridDim.x, g = blockIdx.x;
+    const int64_t u0 = sk_bound(g, U, G), u1 = sk_bound(g + 1, U, G);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool producer = (threadIdx.x == 0);
+    uint64_t pol = 0;
+
+    // producer cursor over global k-steps (incremental: no 64-bit division per k-step)
+    int64_t pc_tile = u0 / KT;
+    int pc_k = (int)(u0 - pc_tile * KT);
+    int pc_m0 = 0, pc_n0 = 0;
+    auto pc_coords = [&]() {
+        int tm, tn;
+        tile_coords((int)pc_tile, tiles_m, tiles_n, group_m, tm, tn);
+        pc_m0 = tm * C::BM;
+        pc_n0 = tn * C::BN;
+    };
+    auto issue_next = [&](int slot) {   // load the cursor's k-step into ring slot, advance
+        tma_issue_stage<C>(base_ptr + slot * C::STAGE_BYTES, &tmA, &tmB, &full[slot], pc_m0, pc_n0, pc_k, pol);
+        if (++pc_k == KT) {
+            pc_k = 0;
+            if (++pc_tile < (int64_t)tiles_m * tiles_n) pc_coords();
+        }
+    };
+    const int nloc = (int)(u1 - u0);   // k-steps of this CTA
+
+    if (producer) {
+#pragma unroll
+        for (int s = 0; s < C::STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], C::CONSUMER_WARPS);
+        }
+        fence_mbar_init();
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+        pol = l2_policy_evict_normal();
+        pc_coords();
+        for (int s = 0; s < C::STAGES && s < nloc; ++s) issue_next(s);
+    }
+    __syncthreads();
+
+    const int warp_m = warp / C::WARPS_N, warp_n = warp % C::WARPS_N;
+    const FragOffsets<C> fo(warp_m, warp_n, lane);
+    double acc[C::MB][C::NP][2][2];
+    int li = 0;                 // local k-step index
+    int stage = 0, phase = 0;   // ring position of li
+    int64_t tile = u0 / KT;
+    int kb = (int)(u0 - tile * KT);
+    while (li < nloc) {
+        const int ke = (int)((u1 - tile * KT) < KT ? (u1 - tile * KT) : KT);
+#pragma unroll
+        for (int mb = 0; mb < C::MB; ++mb)
+#pragma unroll
+            for (int np = 0; np < C::NP; ++np)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) acc[mb][np][j][0] = acc[mb][np][j][1] = 0.0;
+        for (int k = kb; k < ke; ++k, ++li) {
+            if (producer && li > 0 && li - 1 + C::STAGES < nloc) {
+                // refill the slot released at li-1 (the one before `stage`)
+                const int sp = stage == 0 ? C::STAGES - 1 : stage - 1;
+                const int pp = stage == 0 ? phase ^ 1 : phase;
+                mbar_wait(&empty[sp], (uint32_t)pp);
+                issue_next(sp);
+            }
+            mbar_wait(&full[stage], (uint32_t)phase);
+            const uint32_t sA = base + stage * C::STAGE_BYTES;
+            mma_stage<C>(sA, sA + C::A_BYTES, fo, acc);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (++stage == C::STAGES) {
+                stage = 0;
+                phase ^= 1;
+            }
+        }
+        // segments of this tile: CTA boundaries strictly inside (tile*KT, (tile+1)*KT)
+        const int64_t t0 = tile * KT;
+        const int64_t before = sk_count_le(t0, U, G);                  // boundaries <= t0
+        const int nseg = (int)(sk_count_le(t0 + KT - 1, U, G) - before) + 1;
+        int tm, tn;
+        tile_coords((int)tile, tiles_m, tiles_n, group_m, tm, tn);
+        bool do_epi = true;
+        if (nseg > 1) {
+            // Partial of CTA g goes to workspace slot 2g (its first unit) or 2g+1 (its last
+            // unit); segment j of the tile comes from CTA g_j = before - 1 + j.
+            const int64_t my_slot = 2 * g + ((tile * KT + kb) == u0 ? 0 : 1);
+            do_epi = streamk_reduce<C>(acc, ws, counters, tile, my_slot, t0, before, nseg, U, G, warp, lane);
+        }
+        if (do_epi)
+            epilogue<C>(acc, tm * C::BM + warp_m * C::WM, tn * C::BN + warp_n * C::WN, lane, M, N, alpha, beta, Cm,
+                        ldc, vec != 0);
+        ++tile;
+        kb = 0;
+    }
 }
 
 // ------------------------------------------------------------------------------

@@ -246,6 +246,7 @@ static const Cand k_tma_cands[] = {
     {"tma_64x64x16_w32x16_s6_splitk", 0.950},  {"tma_128x64x16_w32x16_s6_splitk", 0.945},
     {"tma_64x128x16_w32x64_s4_splitk", 0.965}, {"tma_128x128x16_w32x32_s4_splitk", 0.960},
 };
+// (stream-K configurations are reached through the tuned table / explicit cfg ids)
 
 struct Choice {
     int id = -1;
@@ -274,7 +275,8 @@ struct PlanKey {
     }
 };
 static std::mutex g_plan_mu;
-static std::map<PlanKey, Choice> g_plans;
+static std::map<PlanKey, Choice> g_plans;    // model plans cached per device
+static std::map<PlanKey, Choice> g_pinned;   // tuner-pinned plans (dev field unused: any device)
 
 static Choice choose(int64_t M, int64_t N, int64_t K, bool tma) {
     int dev = -1;
@@ -285,6 +287,8 @@ static Choice choose(int64_t M, int64_t N, int64_t K, bool tma) {
     const PlanKey key{dev, M, N, K, tma};
     {
         std::lock_guard<std::mutex> lk(g_plan_mu);
+        auto pin = g_pinned.find(PlanKey{0, M, N, K, tma});
+        if (pin != g_pinned.end()) return pin->second;
         auto it = g_plans.find(key);
         if (it != g_plans.end()) return it->second;
     }
@@ -382,6 +386,22 @@ static double *get_pack_buf(cudaStream_t st, int which, size_t doubles) {
         w.pack_cap[which] = doubles;
     }
     return w.pack[which];
+}
+
+static int get_split_ws(cudaStream_t st, size_t doubles, size_t tiles, double **ws, int **ctr);
+
+int streamk_workspace(cudaStream_t st, size_t slot_doubles, int grid, size_t tiles, double **ws, int **ctr) {
+    return get_split_ws(st, slot_doubles * 2 * (size_t)grid, tiles, ws, ctr);
+}
+
+int streamk_grid(const void *kernel, int threads, int smem, int64_t units) {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem) != cudaSuccess || occ < 1) {
+        cudaGetLastError();
+        return -1;
+    }
+    const int64_t g = (int64_t)num_sms() * occ;
+    return (int)(g < units ? g : units);   // >= 1 k-step per CTA keeps CTA boundaries distinct
 }
 
 static int get_split_ws(cudaStream_t st, size_t doubles, size_t tiles, double **ws, int **ctr) {
@@ -524,8 +544,9 @@ int gemm_impl(int64_t M, int64_t N, int64_t K, double alpha, const double *A, in
     if (rc) return rc;
     const gemm_cfg_desc &d = g_cfgs[id].d;
     if (force_splits < 0) return set_error(GEMM_ERR_ARG, "splits=%d must be >= 0", force_splits);
-    if (cfg_id >= 0 && d.split_k != 1) splits = force_splits > 0 ? force_splits : auto_splits(id, M, N, K);
-    if (force_splits > 1 && d.split_k == 1)
+    if (cfg_id >= 0 && d.split_k == 0) splits = force_splits > 0 ? force_splits : auto_splits(id, M, N, K);
+    if (d.split_k == -1) splits = 1;   // stream-K: the work split is fixed by the grid, not by S
+    if (force_splits > 1 && d.split_k != 0)
         return set_error(GEMM_ERR_UNSUPPORTED, "cfg %s has no split-K (use a *_splitk configuration)", g_cfgs[id].name);
     if (splits > 4096) return set_error(GEMM_ERR_ARG, "splits=%d > 4096", splits);
     SplitArgs sk{1, nullptr, nullptr};
@@ -597,22 +618,18 @@ int gemm_plan_set(int64_t M, int64_t N, int64_t K, int tma, int cfg_id, int spli
         return set_error(GEMM_ERR_ARG, "cfg %s has no split-K", g_cfgs[cfg_id].name);
     if (g_cfgs[cfg_id].d.tma && !tma)
         return set_error(GEMM_ERR_ARG, "cfg %s is a TMA configuration but tma=0", g_cfgs[cfg_id].name);
-    int dev = -1;
-    if (cudaGetDevice(&dev) != cudaSuccess) {
-        cudaGetLastError();
-        dev = -1;
-    }
     Choice c;
     c.id = cfg_id;
     c.splits = splits;
     std::lock_guard<std::mutex> lk(g_plan_mu);
-    g_plans[PlanKey{dev, M, N, K, tma != 0}] = c;
+    g_pinned[PlanKey{0, M, N, K, tma != 0}] = c;
     return GEMM_OK;
 }
 
 int gemm_plan_clear(void) {
     std::lock_guard<std::mutex> lk(g_plan_mu);
     g_plans.clear();
+    g_pinned.clear();
     return GEMM_OK;
 }
 

@@ -56,6 +56,38 @@ static int launch_generic(const LaunchArgs &a, cudaStream_t st) {
     return cuda_check(cudaGetLastError(), "dgemm_generic_kernel launch");
 }
 
+// Stream-K launch: grid = min(U, SMs x resident CTAs); workspace = 2 partial slots per CTA.
+int streamk_workspace(cudaStream_t st, size_t slot_doubles, int grid, size_t tiles, double **ws, int **ctr);
+int streamk_grid(const void *kernel, int threads, int smem, int64_t units);
+
+template <class C>
+static int launch_streamk(const LaunchArgs &a, cudaStream_t st) {
+    CUtensorMap ta, tb;
+    int rc = make_tmap(&ta, a.A, a.M, a.K, a.lda, C::BM);
+    if (rc) return rc;
+    rc = make_tmap(&tb, a.B, a.K, a.N, a.ldb, 16);
+    if (rc) return rc;
+    const int64_t tiles = ((int64_t)a.M + C::BM - 1) / C::BM * (((int64_t)a.N + C::BN - 1) / C::BN);
+    const int64_t KT = ((int64_t)a.K + C::BK - 1) / C::BK;
+    const int grid = streamk_grid((const void *)dgemm_streamk_kernel<C>, C::CONSUMER_THREADS, C::SMEM_BYTES,
+                                  tiles * KT);
+    if (grid <= 0) return set_error(GEMM_ERR_CUDA, "stream-K occupancy query failed");
+    double *ws = nullptr;
+    int *ctr = nullptr;
+    rc = streamk_workspace(st, (size_t)C::BM * C::BN, grid, (size_t)tiles, &ws, &ctr);
+    if (rc) return rc;
+    dgemm_streamk_kernel<C><<<grid, C::CONSUMER_THREADS, C::SMEM_BYTES, st>>>(
+        ta, tb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec, a.group_m, ws, ctr);
+    return cuda_check(cudaGetLastError(), "dgemm_streamk_kernel launch");
+}
+
+#define DG_SK(BM, BN, BK, WM, WN, ST)                                                                        \
+    CfgEntry{"tma_" #BM "x" #BN "x" #BK "_w" #WM "x" #WN "_s" #ST "_streamk",                                 \
+             gemm_cfg_desc{BM, BN, BK, WM, WN, ST, Cfg<BM, BN, BK, WM, WN, ST>::CONSUMER_THREADS,              \
+                           (int)Cfg<BM, BN, BK, WM, WN, ST>::SMEM_BYTES, 1, -1, 0},                           \
+             (const void *)dgemm_streamk_kernel<Cfg<BM, BN, BK, WM, WN, ST>>,                                 \
+             launch_streamk<Cfg<BM, BN, BK, WM, WN, ST>>}
+
 #define DG_TMA_SK(BM, BN, BK, WM, WN, ST, SK, SPLIT, XP, SUFFIX)                                              \
     CfgEntry{"tma_" #BM "x" #BN "x" #BK "_w" #WM "x" #WN "_s" #ST SUFFIX,                                     \
              gemm_cfg_desc{BM, BN, BK, WM, WN, ST, Cfg<BM, BN, BK, WM, WN, ST>::CONSUMER_THREADS,              \

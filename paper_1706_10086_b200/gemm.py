@@ -85,6 +85,15 @@ def _load():
 
 _lib = _load()
 
+# The tuned plan table shipped with the package (produced on a B200 by
+# `python -m paper_1706_10086_b200.tuner`); pinned plans override the size model for
+# exactly these shapes.  Set GEMM_F64_NO_TUNED=1 to use the model alone.
+TUNED_TABLE = os.path.join(_HERE, "tuned_b200.txt")
+if os.path.exists(TUNED_TABLE) and not os.environ.get("GEMM_F64_NO_TUNED"):
+    _n = ctypes.c_int()
+    if _lib.gemm_tune_load(os.fsencode(TUNED_TABLE), ctypes.byref(_n)) != 0:
+        raise ImportError(f"bad tuning table {TUNED_TABLE}: {_lib.gemm_last_error().decode()}")
+
 
 def lib():
     return _lib

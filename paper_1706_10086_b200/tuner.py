@@ -34,7 +34,7 @@ def candidates(M: int, N: int, K: int, tma: bool = True):
     for info in G.cfgs():
         if bool(info["tma"]) != tma:
             continue
-        if info["split_k"] == 1:
+        if info["split_k"] != 0:
             out.append((info["id"], 1))
         else:
             kt = (K + info["bk"] - 1) // info["bk"]

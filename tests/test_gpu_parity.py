@@ -130,9 +130,11 @@ def test_all_cfgs_bitwise_identical_and_deterministic(cuda_lib):
     """Every configuration sums each entry in the same order (16-deep k-groups ascending,
     same k-permutation, same DMMA chain) -> identical bits; and runs repeat bitwise."""
     A, B, C0 = synth.problem(334, 290, 778, seed=3)
-    # split-K configurations with one slice run the same chain as the others
-    outs = [run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=c, splits=1) for c in all_cfgs(cuda_lib)]
-    for c, o in zip(all_cfgs(cuda_lib), outs):
+    # split-K configurations with one slice run the same chain as the others; stream-K
+    # cuts tiles between CTAs (a different association) and is checked separately
+    ids = [c["id"] for c in cuda_lib.cfgs() if c["split_k"] != -1]
+    outs = [run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=c, splits=1) for c in ids]
+    for c, o in zip(ids, outs):
         assert np.array_equal(o, outs[0]), cuda_lib.cfg_name(c)
     again = run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=0)
     assert np.array_equal(again, outs[0])
@@ -141,7 +143,11 @@ def test_all_cfgs_bitwise_identical_and_deterministic(cuda_lib):
 
 # ---------------------------------------------------------------- split-K (row a5)
 def split_cfgs(G):
-    return [c["id"] for c in G.cfgs() if c["split_k"] != 1]
+    return [c["id"] for c in G.cfgs() if c["split_k"] == 0]
+
+
+def streamk_cfgs(G):
+    return [c["id"] for c in G.cfgs() if c["split_k"] == -1]
 
 
 @pytest.mark.parametrize("shape", [(70, 90, 1000), (256, 256, 256), (129, 200, 777), (64, 64, 16), (31, 33, 2000)],
@@ -198,6 +204,30 @@ def test_small_sizes_heuristic_plan(cuda_lib, n):
     """The product's own choice (possibly split-K) on config-1/2-like small sizes."""
     A, B, C0 = synth.problem(n, n, n, seed=n)
     check_vs_oracle(run_gpu(cuda_lib, A, B, C0, 1.0, 0.0), A, B, C0, 1.0, 0.0)
+
+
+@pytest.mark.parametrize("shape", [(64, 64, 16), (70, 90, 1000), (256, 256, 256), (129, 200, 778), (1024, 1024, 1024),
+                                   (300, 2000, 64), (2048, 2048, 2048)], ids=lambda s: "x".join(map(str, s)))
+def test_stream_k_within_bound_and_deterministic(cuda_lib, shape):
+    """Stream-K: tiles cut between CTAs are finished by a segment-ordered reduction."""
+    M, N, K = shape
+    A, B, C0 = synth.problem(M, N, K, seed=M + 3)
+    for cfg in streamk_cfgs(cuda_lib):
+        C = run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=cfg)
+        check_vs_oracle(C, A, B, C0, 1.5, 0.5)
+        assert np.array_equal(C, run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=cfg)), cuda_lib.cfg_name(cfg)
+
+
+def test_stream_k_exact_regime_bitwise_and_counters_reset(cuda_lib):
+    A, B, C0 = synth.problem(700, 650, 1300, mode="dyadic", seed=6)
+    ref = oracle.dgemm(1.5, A, B, 0.5, C0)
+    dA, dB = dev(A), dev(B)
+    for cfg in streamk_cfgs(cuda_lib):
+        for _ in range(5):
+            dC = dev(C0)
+            cuda_lib.gemm(dA, dB, dC, 1.5, 0.5, cfg=cfg)
+            torch.cuda.synchronize()
+            assert np.array_equal(dC.cpu().numpy(), ref), cuda_lib.cfg_name(cfg)
 
 
 # ---------------------------------------------------------------- layout / padding

@@ -211,7 +211,7 @@ def small(a):
             for info in G.cfgs():
                 if not info["tma"]:
                     continue
-                for S in ((1,) if info["split_k"] == 1 else (1, 2, 3, 4, 6, 8, 12)):
+                for S in ((1,) if info["split_k"] != 0 else (1, 2, 3, 4, 6, 8, 12)):
                     tb, tm, mhz, pw = P.time(info["id"], a.alpha, a.beta, a.reps, splits=S)
                     r = row(P, info["id"], a.alpha, a.beta, tb, tm, mhz, pw, float("nan"), False, S)
                     w.writerow(r)
