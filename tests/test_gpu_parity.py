@@ -377,6 +377,57 @@ def test_n16384_dyadic_sampled_rows_bitwise(cuda_lib):
     torch.cuda.empty_cache()
 
 
+def test_config4_row_sharded_p8_equals_full(cuda_lib):
+    """Config 4 (M=32768, N=K=4096) row-sharded over P=8 ranks, run rank by rank on one GPU:
+    every rank's shard equals the same rows of the unsharded GEMM bitwise (no split-K)."""
+    M, N, K = 32768, 4096, 4096
+    dA = torch.empty((M, K), dtype=torch.float64, device="cuda")
+    dB = torch.empty((K, N), dtype=torch.float64, device="cuda")
+    dC = torch.empty((M, N), dtype=torch.float64, device="cuda")
+    cuda_lib.fill(dA, "uniform", 1706, 0)
+    cuda_lib.fill(dB, "uniform", 1706, 1)
+    cuda_lib.gemm(dA, dB, dC, 1.0, 0.0, splits=1)
+    for r in range(8):
+        r0, r1 = cuda_lib.row_range(M, r, 8)
+        part = torch.empty((r1 - r0, N), dtype=torch.float64, device="cuda")
+        cuda_lib.gemm(dA[r0:r1], dB, part, 1.0, 0.0, splits=1)
+        torch.cuda.synchronize()
+        assert torch.equal(part, dC[r0:r1]), r
+    torch.cuda.synchronize()
+    rows = _rows(M, bm=4096, extra=4)
+    B = synth.matrix("uniform", 1706, 1, K, N)
+    A_r = np.vstack([synth.matrix("uniform", 1706, 0, M, K, row0=r, nrows=1) for r in rows])
+    ref, mag = oracle.dgemm(1.0, A_r, B, 0.0, np.zeros((len(rows), N)), want_mag=True)
+    res = oracle.check(dC[torch.tensor(rows, device="cuda")].cpu().numpy(), ref, oracle.bound(K, 1.0, 0.0, mag, None))
+    assert res.ok, str(res)
+    del dA, dB, dC
+    torch.cuda.empty_cache()
+
+
+def test_config5_one_rank_shard_sampled(cuda_lib):
+    """Config 5 at full size for one rank of the 8-GPU weak-scaled run: 8192 rows of the
+    N=65536 problem (A 4 GiB, B 32 GiB, C 4 GiB), checked on sampled rows x a 512-column
+    block against the oracle (the largest shape the library is run on)."""
+    M, N, K = 8192, 65536, 65536
+    dA = torch.empty((M, K), dtype=torch.float64, device="cuda")
+    dB = torch.empty((K, N), dtype=torch.float64, device="cuda")
+    dC = torch.empty((M, N), dtype=torch.float64, device="cuda")
+    cuda_lib.fill(dA, "uniform", 1706, 0, rows=65536, row0=0)
+    cuda_lib.fill(dB, "uniform", 1706, 1)
+    cuda_lib.gemm(dA, dB, dC, 1.0, 0.0)
+    torch.cuda.synchronize()
+    c0, nc = 40960, 512
+    rows = [0, 1, 255, 256, 4095, 8191]
+    B = synth.matrix("uniform", 1706, 1, K, N, col0=c0, ncols=nc)
+    A_r = np.vstack([synth.matrix("uniform", 1706, 0, 65536, K, row0=r, nrows=1) for r in rows])
+    ref, mag = oracle.dgemm(1.0, A_r, B, 0.0, np.zeros((len(rows), nc)), want_mag=True)
+    got = dC[torch.tensor(rows, device="cuda")][:, c0:c0 + nc].cpu().numpy()
+    res = oracle.check(got, ref, oracle.bound(K, 1.0, 0.0, mag, None))
+    assert res.ok, str(res)
+    del dA, dB, dC
+    torch.cuda.empty_cache()
+
+
 # ---------------------------------------------------------------- host entry point (e2e)
 def test_host_entry_point(cuda_lib):
     A, B, C0 = synth.problem(700, 650, 300, seed=4)
