@@ -92,15 +92,18 @@ static int host_impl(int64_t M, int64_t N, int64_t K, double alpha, const double
     const bool tiny = !need_ab || flops < 2e10;      // < ~1 ms of GPU work: one shot
     int64_t R0 = M, Rp = M, cb = N;                  // first panel rows, later panel rows, column block
     if (!tiny) {
-        R0 = std::min<int64_t>(M, 2560);             // ~4 * 30 TFLOP/s / 53 GB/s = 2260 rows, rounded up
+        // R0 ~ 4 * compute rate / H2D bandwidth rows keeps the GPU busy while B streams in;
+        // 2304 = 9 rows of 256-row tiles: with 2048-column blocks (32 tiles of 64) a block is
+        // 288 tiles = 1.95 waves of 148 SMs (2560 rows gave 320 tiles = 2.16 waves).
+        R0 = std::min<int64_t>(M, 2304);
         Rp = 2048;
-        cb = std::max<int64_t>(512, ((N + 7) / 8 + 15) / 16 * 16);   // <= 8 column blocks
+        cb = std::max<int64_t>(512, ((N + 7) / 8 + 63) / 64 * 64);   // <= 8 column blocks
     }
     const int64_t ncb = (N + cb - 1) / cb;
     const int64_t nrest = (M > R0) ? (M - R0 + Rp - 1) / Rp : 0;
     // events: one per column block of panel 0, one per later panel, one per column block
     // of the last panel (h2d_done / comp_done each use at most this many)
-    const size_t nev = (size_t)(2 * ncb + nrest + 2);
+    const size_t nev = (size_t)(2 * ncb + nrest + 8);
     if ((rc = ensure_events(P.ev_in, nev))) return rc;
     if ((rc = ensure_events(P.ev_out, nev))) return rc;
 
@@ -154,9 +157,13 @@ static int host_impl(int64_t M, int64_t N, int64_t K, double alpha, const double
         if (need_ab && (rc = h2d_rows(P.dA + r0 * K, K, A + r0 * lda, lda, K, nr, "H2D A panel"))) return rc;
         if (need_c_in && (rc = h2d_rows(P.dC + r0 * N, N, C + r0 * ldc, ldc, N, nr, "H2D C panel"))) return rc;
         if ((rc = h2d_done())) return rc;
+        // the last panel in 2 column blocks: the final D2H overlaps the first one (narrower
+        // blocks shorten the exposed copy but fall into partial waves, measured slower)
         const bool last = (p == nrest - 1);
-        for (int64_t j = 0; j < (last ? ncb : 1); ++j) {
-            const int64_t c0 = last ? j * cb : 0, nc = last ? std::min(N, c0 + cb) - c0 : N;
+        const int64_t lcb = last ? std::max<int64_t>(512, ((N + 1) / 2 + 63) / 64 * 64) : N;
+        const int64_t nlcb = (N + lcb - 1) / lcb;
+        for (int64_t j = 0; j < nlcb; ++j) {
+            const int64_t c0 = j * lcb, nc = std::min(N, c0 + lcb) - c0;
             if ((rc = run(r0, nr, c0, nc))) return rc;
             if ((rc = comp_done())) return rc;
             if ((rc = d2h_block(r0, nr, c0, nc))) return rc;
