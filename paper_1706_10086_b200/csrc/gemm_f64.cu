@@ -245,8 +245,8 @@ static const Cand k_tma_cands[] = {
     {"tma_128x128x16_w32x32_s4", 0.965},       {"tma_64x64x16_w32x16_s6", 0.952},
     {"tma_64x64x16_w32x16_s6_splitk", 0.950},  {"tma_128x64x16_w32x16_s6_splitk", 0.945},
     {"tma_64x128x16_w32x64_s4_splitk", 0.965}, {"tma_128x128x16_w32x32_s4_splitk", 0.960},
+    {"tma_128x64x16_w32x16_s6_streamk", 0.935}, {"tma_64x64x16_w32x16_s6_streamk", 0.920},
 };
-// (stream-K configurations are reached through the tuned table / explicit cfg ids)
 
 struct Choice {
     int id = -1;
@@ -263,43 +263,48 @@ static double est_time(const gemm_cfg_desc &d, int occ, int sms, int64_t M, int6
     return (double)waves * occ * d.bm * d.bn * ksteps * (d.bk / 16.0) / eff;
 }
 
-static Choice choose_uncached(int64_t M, int64_t N, int64_t K, bool tma);
+static Choice choose_uncached(int64_t M, int64_t N, int64_t K, bool tma, bool single_pass);
 
 // Plans are cached per (device, M, N, K, TMA-eligible).
 struct PlanKey {
     int dev;
     int64_t M, N, K;
     bool tma;
+    bool single_pass = false;   // plans restricted to one k-pass per tile (no split-K / stream-K)
     bool operator<(const PlanKey &o) const {
-        return std::tie(dev, M, N, K, tma) < std::tie(o.dev, o.M, o.N, o.K, o.tma);
+        return std::tie(dev, M, N, K, tma, single_pass) < std::tie(o.dev, o.M, o.N, o.K, o.tma, o.single_pass);
     }
 };
 static std::mutex g_plan_mu;
 static std::map<PlanKey, Choice> g_plans;    // model plans cached per device
 static std::map<PlanKey, Choice> g_pinned;   // tuner-pinned plans (dev field unused: any device)
 
-static Choice choose(int64_t M, int64_t N, int64_t K, bool tma) {
+// single_pass: only plans whose per-entry arithmetic is the plain one-pass k chain (used by
+// the row-panel / column-panel paths that promise bits identical to a one-shot call).
+static Choice choose(int64_t M, int64_t N, int64_t K, bool tma, bool single_pass = false) {
     int dev = -1;
     if (cudaGetDevice(&dev) != cudaSuccess) {
         cudaGetLastError();
         dev = -1;
     }
-    const PlanKey key{dev, M, N, K, tma};
+    const PlanKey key{dev, M, N, K, tma, single_pass};
     {
         std::lock_guard<std::mutex> lk(g_plan_mu);
         auto pin = g_pinned.find(PlanKey{0, M, N, K, tma});
-        if (pin != g_pinned.end()) return pin->second;
+        if (pin != g_pinned.end() &&
+            (!single_pass || (g_cfgs[pin->second.id].d.split_k != -1 && pin->second.splits == 1)))
+            return pin->second;
         auto it = g_plans.find(key);
         if (it != g_plans.end()) return it->second;
     }
-    const Choice c = choose_uncached(M, N, K, tma);
+    const Choice c = choose_uncached(M, N, K, tma, single_pass);
     std::lock_guard<std::mutex> lk(g_plan_mu);
     if (g_plans.size() > 4096) g_plans.clear();
     g_plans[key] = c;
     return c;
 }
 
-static Choice choose_uncached(int64_t M, int64_t N, int64_t K, bool tma) {
+static Choice choose_uncached(int64_t M, int64_t N, int64_t K, bool tma, bool single_pass) {
     Choice best;
     if (!tma) {
         const int64_t tiles128 = ((M + 127) / 128) * ((N + 127) / 128);
@@ -318,6 +323,18 @@ static Choice choose_uncached(int64_t M, int64_t N, int64_t K, bool tma) {
         }
         const gemm_cfg_desc &d = g_cfgs[id].d;
         const int64_t KT = (K + d.bk - 1) / d.bk;
+        if (single_pass && d.split_k != 1) continue;
+        if (d.split_k == -1) {   // stream-K: every CTA gets ceil(U/G) k-steps, no partial waves
+            const int64_t tiles = ((M + d.bm - 1) / d.bm) * ((N + d.bn - 1) / d.bn);
+            const int64_t G = std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * occ, tiles * KT));
+            const double t = ((double)((tiles * KT + G - 1) / G) + 6.0) * occ * d.bm * d.bn * (d.bk / 16.0) / c.eff;
+            if (t < best_t * 0.999) {
+                best_t = t;
+                best.id = id;
+                best.splits = 1;
+            }
+            continue;
+        }
         const int smax = d.split_k == 1 ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(16, KT / 4));
         for (int S = 1; S <= smax; ++S) {
             const double t = est_time(d, occ, sms, M, N, K, S, c.eff);
@@ -531,9 +548,9 @@ int gemm_impl(int64_t M, int64_t N, int64_t K, double alpha, const double *A, in
     int id = cfg_id;
     int splits = 1;
     if (id < 0) {
-        const Choice c = choose(M, N, K, tma);
+        const Choice c = choose(M, N, K, tma, force_splits == 1);   // 1: one k-pass per tile
         id = c.id;
-        splits = force_splits == 1 ? 1 : c.splits;   // 1: heuristic tile, no split-K
+        splits = force_splits == 1 ? 1 : c.splits;
     } else if (g_cfgs[id].d.tma && !tma) {
         return set_error(GEMM_ERR_UNSUPPORTED,
                          "cfg %s needs 16-byte aligned A/B and even lda/ldb (A%%16=%d B%%16=%d lda=%lld ldb=%lld)",
