@@ -505,3 +505,29 @@ def test_peak_probe_runs(cuda_lib):
     cuda_lib.peak_probe("dfma", 148, 8, 1000, out, cyc)
     torch.cuda.synchronize()
     assert int(cyc.item()) > 0
+
+
+# ---------------------------------------------------------------- CUDA graphs
+def test_cuda_graph_capture_and_replay(cuda_lib):
+    """The C-ABI calls are capturable after a warm-up call on the stream (workspace and tensor
+    maps exist): a graph of 20 small GEMMs (split-K plan, config-1 size) replays with the same
+    bits as eager launches."""
+    n = 256
+    A, B, C0 = synth.problem(n, n, n, seed=21)
+    dA, dB = dev(A), dev(B)
+    outs = [torch.zeros((n, n), dtype=torch.float64, device="cuda") for _ in range(20)]
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        cuda_lib.gemm(dA, dB, outs[0], 1.0, 0.0)     # warm-up: workspace, plan, tensor maps
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for o in outs:
+            cuda_lib.gemm(dA, dB, o, 1.0, 0.0)
+    for o in outs:
+        o.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    eager = run_gpu(cuda_lib, A, B, C0, 1.0, 0.0)
+    for o in outs:
+        assert np.array_equal(o.cpu().numpy(), eager)
