@@ -255,6 +255,208 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): a cluster of 2 CTAs on one TPC computes a 256 x BN tile
+// with M=256 UMMAs issued by the leader CTA.  Each CTA stages its own 128 rows of A and its
+// half (BN/2 rows) of B^T; the pair's tensor cores read both halves, so the shared-memory
+// operand traffic per SM is A 4 KB + B 4 KB per K=8 step instead of 4 + 8 KB at N=256 on one
+// SM.  Both CTAs' TMA bytes complete on the leader's full barrier (arrivals: leader
+// expect_tx + peer remote arrive); the leader's tcgen05.commit multicasts to both CTAs'
+// empty / accumulator barriers; each CTA's epilogue reads its own 128 TMEM lanes.
+template <int BN_, int BK_, int STAGES_>
+struct Cfg2 {
+    static constexpr int BN = BN_, BK = BK_, STAGES = STAGES_, BN_HALF = BN_ / 2;
+    static_assert(BN % 32 == 0 && BN >= 64 && BN <= 256, "UMMA N for M=256 (2 CTAs): multiple of 16, <= 256");
+    static_assert(BK == 32 || BK == 16, "k-stage row = one 128-byte or 64-byte swizzle row");
+    static constexpr uint32_t SBO = 8 * BK * 4;
+    static constexpr uint32_t LAYOUT = BK == 32 ? 2u : 4u;
+    static constexpr uint32_t A_BYTES = 128 * BK * 4;        // this CTA's 128 rows, one of hi / lo
+    static constexpr uint32_t B_BYTES = BN_HALF * BK * 4;    // this CTA's half of B^T, one of hi / lo
+    static constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+    static constexpr uint32_t TMEM_COLS = (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
+    static constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+    static constexpr int THREADS = 192;
+};
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_remote_arrive(uint64_t *bar, uint32_t cta) {
+    asm volatile(
+        "{\n"
+        ".reg .b32 ra;\n"
+        "mapa.shared::cluster.u32 ra, %0, %1;\n"
+        "mbarrier.arrive.shared::cluster.b64 _, [ra];\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(cta)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(void *smem_dst, const CUtensorMap *map, int c0, int c1,
+                                                 uint64_t *leader_bar_local) {
+    // the mbarrier address with the peer bit cleared names the leader CTA's barrier
+    const uint32_t bar = smem_u32(leader_bar_local) & 0xFEFFFFFFu;
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void umma_tf32_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                               uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit_pair(uint64_t *bar) {
+    const uint16_t mask = 0x3;
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
+
+template <class C>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C::THREADS, 1)
+    sgemm_3xtf32_2sm_kernel(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
+                            const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl, int M,
+                            int N, int K, float alpha, float beta, float *__restrict__ Cm, int64_t ldc, int group_m) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t *base_ptr = smem_raw + (base - raw);
+    uint64_t *full = reinterpret_cast<uint64_t *>(base_ptr + C::STAGES * C::STAGE_BYTES);
+    uint64_t *empty = full + C::STAGES;
+    uint64_t *tmem_full = empty + C::STAGES;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
+
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = (rank == 0);
+    const int tiles_m = (M + 255) / 256, tiles_n = (N + C::BN - 1) / C::BN;
+    int tm, tn;
+    tile_coords(blockIdx.x >> 1, tiles_m, tiles_n, group_m, tm, tn);
+    const int my_m0 = tm * 256 + (int)rank * 128;          // this CTA's 128 rows of A / C
+    const int n0 = tn * C::BN;
+    const int my_n0 = n0 + (int)rank * C::BN_HALF;          // this CTA's half of B^T
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int BK = C::BK;
+    const int KT = (K + BK - 1) / BK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < C::STAGES; ++s) {
+            mbar_init(&full[s], 2);    // leader's expect_tx arrive + the peer's remote arrive
+            mbar_init(&empty[s], 1);   // the leader's multicast commit
+        }
+        mbar_init(tmem_full, 1);
+        fence_mbar_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                     "n"(C::TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::: "memory");
+    }
+    tc_fence_before();
+    cluster_sync_all();   // both CTAs: barriers initialised, TMEM allocated
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {   // ---------------- TMA producer (both CTAs)
+            tma_prefetch_desc(&tmAh);
+            tma_prefetch_desc(&tmAl);
+            tma_prefetch_desc(&tmBh);
+            tma_prefetch_desc(&tmBl);
+            for (int kt = 0; kt < KT; ++kt) {
+                const int s = kt % C::STAGES;
+                if (kt >= C::STAGES) mbar_wait(&empty[s], ((kt / C::STAGES) - 1) & 1);
+                if (leader)
+                    mbar_arrive_expect_tx(&full[s], 2 * C::STAGE_BYTES);
+                else
+                    mbar_remote_arrive(&full[s], 0);
+                uint8_t *st = base_ptr + s * C::STAGE_BYTES;
+                const int k = kt * BK;
+                tma_load_2d_pair(st, &tmAh, k, my_m0, &full[s]);
+                tma_load_2d_pair(st + C::A_BYTES, &tmAl, k, my_m0, &full[s]);
+                uint8_t *sb = st + 2 * C::A_BYTES;
+                tma_load_2d_pair(sb, &tmBh, k, my_n0, &full[s]);
+                tma_load_2d_pair(sb + C::B_BYTES, &tmBl, k, my_n0, &full[s]);
+            }
+        }
+    } else if (warp == 1) {
+        if (leader && lane == 0) {   // ---------------- MMA issuer (leader CTA only)
+            constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(C::BN >> 3) << 17) |
+                                       ((uint32_t)(256 >> 4) << 24);
+            for (int kt = 0; kt < KT; ++kt) {
+                const int s = kt % C::STAGES;
+                mbar_wait(&full[s], (kt / C::STAGES) & 1);
+                tc_fence_after();
+                const uint32_t sa = base + s * C::STAGE_BYTES;
+                const uint32_t sb = sa + 2 * C::A_BYTES;
+#pragma unroll
+                for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+                    const uint64_t a_hi = umma_desc(sa + kk * 32, 0, C::SBO, C::LAYOUT);
+                    const uint64_t b_hi = umma_desc(sb + kk * 32, 0, C::SBO, C::LAYOUT);
+                    umma_tf32_pair(tmem, a_hi, b_hi, idesc, (kt > 0 || kk > 0) ? 1u : 0u);
+                }
+#pragma unroll
+                for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+                    const uint64_t a_hi = umma_desc(sa + kk * 32, 0, C::SBO, C::LAYOUT);
+                    const uint64_t a_lo = umma_desc(sa + C::A_BYTES + kk * 32, 0, C::SBO, C::LAYOUT);
+                    const uint64_t b_hi = umma_desc(sb + kk * 32, 0, C::SBO, C::LAYOUT);
+                    const uint64_t b_lo = umma_desc(sb + C::B_BYTES + kk * 32, 0, C::SBO, C::LAYOUT);
+                    umma_tf32_pair(tmem + C::BN, a_lo, b_hi, idesc, (kt > 0 || kk > 0) ? 1u : 0u);
+                    umma_tf32_pair(tmem + C::BN, a_hi, b_lo, idesc, 1u);
+                }
+                umma_commit_pair(&empty[s]);
+            }
+            umma_commit_pair(tmem_full);
+        }
+    } else {
+        // ---------------- epilogue warps 2..5 (both CTAs): own 128 TMEM lanes
+        const int q = warp & 3;
+        mbar_wait(tmem_full, 0);
+        tc_fence_after();
+        const int row = my_m0 + q * 32 + lane;
+        float *crow = Cm + (int64_t)row * ldc;
+        const bool row_ok = row < M;
+#pragma unroll 1
+        for (int c = 0; c < C::BN; c += 16) {
+            uint32_t v[16], w[16];
+            tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
+            tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(C::BN + c), w);
+            if (row_ok) {
+                const int col = n0 + c;
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    if (col + e < N) {
+                        const float acc = __uint_as_float(v[e]) + __uint_as_float(w[e]);
+                        crow[col + e] = (beta != 0.0f) ? fmaf(alpha, acc, beta * crow[col + e]) : alpha * acc;
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();   // the peer's smem / TMEM stay valid until both CTAs are done
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(C::TMEM_COLS)
+                     : "memory");
+    }
+}
+
 // x -> (rn_tf32(x), rn_tf32(x - rn_tf32(x))), packed rows of pitch ldo.
 __global__ void split_tf32_kernel(const float *__restrict__ X, int64_t ldx, int64_t rows, int64_t cols,
                                   float *__restrict__ hi, float *__restrict__ lo, int64_t ldo) {
@@ -317,6 +519,7 @@ struct F32Cfg {
     const void *kernel;
     void (*launch)(dim3, cudaStream_t, const CUtensorMap &, const CUtensorMap &, const CUtensorMap &,
                    const CUtensorMap &, int, int, int, float, float, float *, int64_t, int);
+    int ctas = 1;   // 2: CTA pair (cta_group::2), 256-row tiles
 };
 
 template <class C>
@@ -331,15 +534,31 @@ static void launch_f32(dim3 grid, cudaStream_t st, const CUtensorMap &a, const C
     F32Cfg{"tf32x3_128x" #BN "x" #BK "_s" #ST, BN, BK, ST, Cfg<BN, BK, ST>::SMEM_BYTES,                       \
            (const void *)sgemm_3xtf32_kernel<Cfg<BN, BK, ST>>, launch_f32<Cfg<BN, BK, ST>>}
 
+template <class C>
+static void launch_f32_pair(dim3 grid, cudaStream_t st, const CUtensorMap &a, const CUtensorMap &b,
+                            const CUtensorMap &c, const CUtensorMap &d, int M, int N, int K, float alpha, float beta,
+                            float *Cm, int64_t ldc, int group_m) {
+    sgemm_3xtf32_2sm_kernel<C><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(a, b, c, d, M, N, K, alpha, beta, Cm, ldc,
+                                                                         group_m);
+}
+
+// pair configurations: bm = 256 (two CTAs), the A box is 128 rows, the B box BN/2 rows
+#define F32CFG2(BN, BK, ST)                                                                                  \
+    F32Cfg{"tf32x3_2sm_256x" #BN "x" #BK "_s" #ST, BN, BK, ST, Cfg2<BN, BK, ST>::SMEM_BYTES,                  \
+           (const void *)sgemm_3xtf32_2sm_kernel<Cfg2<BN, BK, ST>>, launch_f32_pair<Cfg2<BN, BK, ST>>, 2}
+
 static const F32Cfg k_f32_cfgs[] = {
     F32CFG(128, 32, 3),
     F32CFG(128, 16, 6),
     F32CFG(256, 32, 2),
     F32CFG(256, 16, 4),
+    F32CFG2(256, 32, 3),
+    F32CFG2(256, 16, 6),
 };
 static constexpr int kNumF32Cfgs = sizeof(k_f32_cfgs) / sizeof(k_f32_cfgs[0]);
 static constexpr int kDefaultF32 = 0;   // tf32x3_128x128x32_s3
-static constexpr int kWideF32 = 3;      // tf32x3_128x256x16_s4 (measured best at 8192 / 16384)
+static constexpr int kWideF32 = 3;      // tf32x3_128x256x16_s4
+static constexpr int kPairF32 = 4;      // tf32x3_2sm_256x256x32_s3 (measured best at 8192 / 16384)
 
 struct Ws {
     float *buf = nullptr;
@@ -405,8 +624,10 @@ static int impl(int64_t M, int64_t N, int64_t K, float alpha, const float *A, in
     }
     if (cfg_id < -1 || cfg_id >= kNumF32Cfgs)
         return set_error(GEMM_ERR_ARG, "f32 cfg_id=%d out of range [-1, %d)", cfg_id, kNumF32Cfgs);
-    // default: 128 x 256 tiles (fewer L2 bytes per FLOP) unless N is small
-    const F32Cfg &cf = k_f32_cfgs[cfg_id >= 0 ? cfg_id : (N > 128 ? kWideF32 : kDefaultF32)];
+    // default: CTA-pair 256 x 256 tiles for large problems (least shared-memory operand
+    // traffic per FLOP), 128 x 256 for medium, 128 x 128 when N is small
+    const int pick = (M >= 512 && N >= 256) ? kPairF32 : (N > 128 ? kWideF32 : kDefaultF32);
+    const F32Cfg &cf = k_f32_cfgs[cfg_id >= 0 ? cfg_id : pick];
     // split A and B into tf32 hi / lo in workspace, row pitch padded to 16 bytes
     const int64_t ka = (K + 3) & ~int64_t(3);
     const size_t a_sz = (size_t)M * ka, b_sz = (size_t)N * ka;   // A and B^T, both K-major
@@ -423,10 +644,11 @@ static int impl(int64_t M, int64_t N, int64_t K, float alpha, const float *A, in
         if (rc) return rc;
     }
     CUtensorMap mAh, mAl, mBh, mBl;
+    const int bbox = cf.ctas == 2 ? cf.bn / 2 : cf.bn;   // B^T rows per CTA
     int rc = make_tmap_f32(&mAh, Ah, M, K, ka, cf.bk, BM);
     if (!rc) rc = make_tmap_f32(&mAl, Al, M, K, ka, cf.bk, BM);
-    if (!rc) rc = make_tmap_f32(&mBh, Bh, N, K, ka, cf.bk, cf.bn);
-    if (!rc) rc = make_tmap_f32(&mBl, Bl, N, K, ka, cf.bk, cf.bn);
+    if (!rc) rc = make_tmap_f32(&mBh, Bh, N, K, ka, cf.bk, bbox);
+    if (!rc) rc = make_tmap_f32(&mBl, Bl, N, K, ka, cf.bk, bbox);
     if (rc) return rc;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -440,7 +662,8 @@ static int impl(int64_t M, int64_t N, int64_t K, float alpha, const float *A, in
             g_attr[key] = true;
         }
     }
-    const int64_t tiles = ((M + BM - 1) / BM) * ((N + cf.bn - 1) / cf.bn);
+    const int64_t bm = (int64_t)BM * cf.ctas;
+    const int64_t tiles = ((M + bm - 1) / bm) * ((N + cf.bn - 1) / cf.bn) * cf.ctas;   // CTAs
     if (tiles > 0x7FFFFFFF) return set_error(GEMM_ERR_UNSUPPORTED, "too many tiles (%lld)", (long long)tiles);
     cf.launch(dim3((unsigned)tiles), st, mAh, mAl, mBh, mBl, (int)M, (int)N, (int)K, alpha, beta, C, ldc, 8);
     return cuda_check(cudaGetLastError(), "sgemm_3xtf32_kernel launch");
