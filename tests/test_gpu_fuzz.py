@@ -1,0 +1,55 @@
+"""Randomised GPU parity (fixed seed, reproducible): shapes, alpha/beta (incl. 0 and 1),
+leading-dimension padding, 8-byte (non-16-byte) pointer offsets and forced configurations,
+all against the CPU oracle within the north-star bound."""
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def _place(x, pad, offset):
+    """Copy x into a device buffer with `pad` extra columns and an 8-byte `offset`."""
+    r, c = x.shape
+    ld = c + pad
+    buf = torch.full((r * ld + offset + 1,), float("nan"), dtype=torch.float64, device="cuda")
+    view = buf[offset:offset + r * ld].view(r, ld)[:, :c] if r > 0 else buf[:0].view(0, c)
+    if r > 0 and c > 0:
+        view.copy_(torch.from_numpy(np.ascontiguousarray(x)))
+    return buf, view
+
+
+@pytest.mark.parametrize("case", range(40))
+def test_random_cases(cuda_lib, case):
+    rng = np.random.default_rng(1000 + case)
+    M, N, K = (int(v) for v in rng.integers(1, 600, 3))
+    if case % 7 == 0:
+        K = int(rng.integers(1, 8))
+    alpha = [1.0, -0.75, 1.5, 0.0][case % 4]
+    beta = [0.0, 1.0, 0.5, -2.0][(case // 4) % 4]
+    A, B, C0 = synth.problem(M, N, K, seed=case)
+    pads = [int(v) for v in rng.integers(0, 3, 3)]
+    offs = [int(v) for v in rng.integers(0, 2, 3)]
+    bufs = [_place(x, p, o) for x, p, o in zip((A, B, C0), pads, offs)]
+    (_, dA), (_, dB), (bC, dC) = bufs
+    cfg = None
+    if case % 3 == 1:   # force a configuration the inputs are eligible for
+        tma_ok = all(o == 0 for o in offs[:2]) and (dA.stride(0) % 2 == 0 or M == 1) and (dB.stride(0) % 2 == 0 or K == 1)
+        cands = [c["id"] for c in cuda_lib.cfgs() if (tma_ok or not c["tma"])]
+        cfg = int(rng.choice(cands))
+    cuda_lib.gemm(dA, dB, dC, alpha, beta, cfg=cfg)
+    torch.cuda.synchronize()
+    ref, mag = oracle.dgemm(alpha, A, B, beta, C0, want_mag=True)
+    res = oracle.check(dC.cpu().numpy(), ref, oracle.bound(K, alpha, beta, mag, C0))
+    assert res.ok, (M, N, K, alpha, beta, pads, offs, cfg, str(res))
+    # nothing outside the C view was touched (padding columns and the offset word stay NaN)
+    full = bC.cpu().numpy()
+    ldc = N + pads[2]
+    mask = np.ones_like(full, dtype=bool)
+    for i in range(M):
+        mask[offs[2] + i * ldc: offs[2] + i * ldc + N] = False
+    assert np.all(np.isnan(full[mask]))
