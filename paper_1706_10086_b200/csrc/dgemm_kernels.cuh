@@ -437,8 +437,8 @@ __device__ __forceinline__ int64_t sk_count_le(int64_t x, int64_t U, int64_t G) 
 
 template <class C>
 __device__ __forceinline__ bool streamk_reduce(double (&acc)[C::MB][C::NP][2][2], double *ws, int *counters,
-                                               int64_t tile, int64_t my_slot, int64_t t0, int64_t before, int nseg,
-                                               int64_t U, int64_t G, int warp, int lane) {
+                                               int tile, int my_slot, int t0, int before, int nseg, int U, int G,
+                                               int warp, int lane) {
     constexpr int Q = C::E / 4;
     constexpr int64_t QSTRIDE = (int64_t)C::CONSUMER_WARPS * 32 * 4;
     double *mine = partial_slot<C>(ws, my_slot, warp, lane);
@@ -455,8 +455,8 @@ __device__ __forceinline__ bool streamk_reduce(double (&acc)[C::MB][C::NP][2][2]
 #pragma unroll
     for (int e = 0; e < C::E; ++e) flat[e] = 0.0;
     for (int j = 0; j < nseg; ++j) {           // segment order = k order
-        const int64_t gj = before - 1 + j;
-        const int64_t slot = 2 * gj + (sk_bound(gj, U, G) >= t0 ? 0 : 1);
+        const int gj = before - 1 + j;
+        const int slot = 2 * gj + (sk_bound(gj, U, G) >= t0 ? 0 : 1);
         const double *src = partial_slot<C>(ws, slot, warp, lane);
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
@@ -487,20 +487,22 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
     uint64_t *empty = full + C::STAGES;
 
     const int tiles_m = (M + C::BM - 1) / C::BM, tiles_n = (N + C::BN - 1) / C::BN;
-    const int64_t KT = (K + C::BK - 1) / C::BK;
-    const int64_t U = (int64_t)tiles_m * tiles_n * KT, G = gridDim.x, g = blockIdx.x;
-    const int64_t u0 = sk_bound(g, U, G), u1 = sk_bound(g + 1, U, G);
+    // 32-bit k-step bookkeeping (the host guarantees U = tiles * KT < 2^31) keeps the
+    // 64x32-warp-tile instance free of register spills
+    const int KT = (K + C::BK - 1) / C::BK;
+    const int U = tiles_m * tiles_n * KT, G = gridDim.x, g = blockIdx.x;
+    const int u0 = (int)sk_bound(g, U, G), u1 = (int)sk_bound(g + 1, U, G);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool producer = (threadIdx.x == 0);
     uint64_t pol = 0;
 
-    // producer cursor over global k-steps (incremental: no 64-bit division per k-step)
-    int64_t pc_tile = u0 / KT;
-    int pc_k = (int)(u0 - pc_tile * KT);
+    // producer cursor over global k-steps (incremental: no division per k-step)
+    int pc_tile = u0 / KT;
+    int pc_k = u0 - pc_tile * KT;
     int pc_m0 = 0, pc_n0 = 0;
     auto pc_coords = [&]() {
         int tm, tn;
-        tile_coords((int)pc_tile, tiles_m, tiles_n, group_m, tm, tn);
+        tile_coords(pc_tile, tiles_m, tiles_n, group_m, tm, tn);
         pc_m0 = tm * C::BM;
         pc_n0 = tn * C::BN;
     };
@@ -508,10 +510,10 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
         tma_issue_stage<C>(base_ptr + slot * C::STAGE_BYTES, &tmA, &tmB, &full[slot], pc_m0, pc_n0, pc_k, pol);
         if (++pc_k == KT) {
             pc_k = 0;
-            if (++pc_tile < (int64_t)tiles_m * tiles_n) pc_coords();
+            if (++pc_tile < tiles_m * tiles_n) pc_coords();
         }
     };
-    const int nloc = (int)(u1 - u0);   // k-steps of this CTA
+    const int nloc = u1 - u0;   // k-steps of this CTA
 
     if (producer) {
 #pragma unroll
@@ -533,10 +535,10 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
     double acc[C::MB][C::NP][2][2];
     int li = 0;                 // local k-step index
     int stage = 0, phase = 0;   // ring position of li
-    int64_t tile = u0 / KT;
-    int kb = (int)(u0 - tile * KT);
+    int tile = u0 / KT;
+    int kb = u0 - tile * KT;
     while (li < nloc) {
-        const int ke = (int)((u1 - tile * KT) < KT ? (u1 - tile * KT) : KT);
+        const int ke = (u1 - tile * KT) < KT ? (u1 - tile * KT) : KT;
 #pragma unroll
         for (int mb = 0; mb < C::MB; ++mb)
 #pragma unroll
@@ -562,16 +564,16 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
             }
         }
         // segments of this tile: CTA boundaries strictly inside (tile*KT, (tile+1)*KT)
-        const int64_t t0 = tile * KT;
-        const int64_t before = sk_count_le(t0, U, G);                  // boundaries <= t0
-        const int nseg = (int)(sk_count_le(t0 + KT - 1, U, G) - before) + 1;
+        const int t0 = tile * KT;
+        const int before = (int)sk_count_le(t0, U, G);                 // boundaries <= t0
+        const int nseg = (int)sk_count_le(t0 + KT - 1, U, G) - before + 1;
         int tm, tn;
-        tile_coords((int)tile, tiles_m, tiles_n, group_m, tm, tn);
+        tile_coords(tile, tiles_m, tiles_n, group_m, tm, tn);
         bool do_epi = true;
         if (nseg > 1) {
             // Partial of CTA g goes to workspace slot 2g (its first unit) or 2g+1 (its last
             // unit); segment j of the tile comes from CTA g_j = before - 1 + j.
-            const int64_t my_slot = 2 * g + ((tile * KT + kb) == u0 ? 0 : 1);
+            const int my_slot = 2 * g + ((t0 + kb) == u0 ? 0 : 1);
             do_epi = streamk_reduce<C>(acc, ws, counters, tile, my_slot, t0, before, nseg, U, G, warp, lane);
         }
         if (do_epi)

@@ -69,6 +69,7 @@ static int launch_streamk(const LaunchArgs &a, cudaStream_t st) {
     if (rc) return rc;
     const int64_t tiles = ((int64_t)a.M + C::BM - 1) / C::BM * (((int64_t)a.N + C::BN - 1) / C::BN);
     const int64_t KT = ((int64_t)a.K + C::BK - 1) / C::BK;
+    if (tiles * KT > 0x7FFFFFFF) return set_error(GEMM_ERR_UNSUPPORTED, "stream-K needs tiles*k-steps < 2^31");
     const int grid = streamk_grid((const void *)dgemm_streamk_kernel<C>, C::CONSUMER_THREADS, C::SMEM_BYTES,
                                   tiles * KT);
     if (grid <= 0) return set_error(GEMM_ERR_CUDA, "stream-K occupancy query failed");

@@ -353,6 +353,32 @@ def test_config3_n8192_alpha_beta_sampled_rows(cuda_lib):
     _sampled_rows_check(cuda_lib, 8192, 8192, 8192, 1.5, 0.5, _rows(8192, extra=6))
 
 
+def test_config3_every_cfg_sampled_rows(cuda_lib):
+    """Config 3 (N=8192, alpha=1.5, beta=0.5): every grid point of the tuning sweep
+    (tools/sweep.py tune times them) passes sampled-row parity."""
+    n = 8192
+    dA = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    dB = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    dC = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    cuda_lib.fill(dA, "uniform", 1706, 0)
+    cuda_lib.fill(dB, "uniform", 1706, 1)
+    rows = _rows(n, extra=3)
+    B = synth.matrix("uniform", 1706, 1, n, n)
+    A_r = np.vstack([synth.matrix("uniform", 1706, 0, n, n, row0=r, nrows=1) for r in rows])
+    C0_r = np.vstack([synth.matrix("uniform", 1706, 2, n, n, row0=r, nrows=1) for r in rows])
+    ref, mag = oracle.dgemm(1.5, A_r, B, 0.5, C0_r, want_mag=True)
+    bnd = oracle.bound(n, 1.5, 0.5, mag, C0_r)
+    idx = torch.tensor(rows, device="cuda")
+    for info in cuda_lib.cfgs():
+        cuda_lib.fill(dC, "uniform", 1706, 2)
+        cuda_lib.gemm(dA, dB, dC, 1.5, 0.5, cfg=info["id"])
+        torch.cuda.synchronize()
+        res = oracle.check(dC[idx].cpu().numpy(), ref, bnd)
+        assert res.ok, (info["name"], str(res))
+    del dA, dB, dC
+    torch.cuda.empty_cache()
+
+
 def test_config2_n16384_sampled_rows_bench_launch(cuda_lib):
     """The bench workload (16384^3, alpha=1, beta=0, heuristic config = bench launch)."""
     _sampled_rows_check(cuda_lib, 16384, 16384, 16384, 1.0, 0.0, _rows(16384, extra=4))
