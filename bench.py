@@ -274,6 +274,8 @@ def main():
     cfg_name = G.cfg_name(cfg if cfg is not None else plan_cfg)
     if cfg is None and plan_splits > 1:
         cfg_name += f" (split-K x{plan_splits})"
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    launches_per_step = G.launches_per_call(cfg if cfg is not None else plan_cfg, Ml, N, K, sms)
 
     def step(evs=None):
         if comm is not None:
@@ -340,6 +342,7 @@ def main():
     roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_DATASHEET_TFLOPS, "unit": "TFLOP/s",
                 "frac": achieved / FP64_DATASHEET_TFLOPS, "traffic": traffic,
                 "kernel": cfg_name, "kernel_ms_mean": k_mean, "flops_per_launch": flops_local,
+                "launches_per_gemm": launches_per_step,
                 "peak_source": "FP64 / FP64-tensor datasheet peak of one HGX B200 GPU (296/8); MEASURED_PEAKS.json has "
                                "no FP64 entry (DESIGN.md §Roofline)"}
     if peaks.get("bf16_tflops"):
@@ -375,7 +378,7 @@ def main():
                            "parallelism": f"row-sharded x{world}, B broadcast (NCCL)" if world > 1 else "1 GPU"},
                 "pct_of_fp64_peak": 100.0 * value / (FP64_DATASHEET_TFLOPS * world),
                 "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": a.steps}
+                "gpu_launches": a.steps * launches_per_step}
         print(json.dumps(line), flush=True)
     if comm is not None:
         comm.close()

@@ -16,6 +16,7 @@ static const CfgEntry k_table[] = {
     DG_TMA(256, 64, 16, 32, 32, 4),
     DG_TMA_XP(256, 64, 16, 64, 32, 4),
     DG_TMA_XP(128, 128, 16, 64, 32, 4),
+    DG_HYB(256, 64, 16, 64, 32, 4),
 };
 
 const CfgEntry *cfg_table_big(int *n) {

@@ -163,7 +163,35 @@ __device__ __forceinline__ void mma_half(const Frag<C> &f, double (&acc)[C::MB][
 
 // Epilogue (row a4): C = alpha*acc + beta*C, each C element read (beta != 0) and written once.
 // Thread (g, t) of an (m-block, n-pair) owns row g and the 4 contiguous columns 4t..4t+3:
-// acc[mb][np][j][i] is real column 4t + 2i + j of the n-pair.
+// acc[mb][np][j][i] is real column 4t + 2i + j of the n-pair; v = {acc[..][0][0],
+// acc[..][1][0], acc[..][0][1], acc[..][1][1]} are columns col..col+3.
+__device__ __forceinline__ void epilogue_quad(const double (&v)[4], int row, int col, int M, int N, double alpha,
+                                              double beta, double *__restrict__ Cm, int64_t ldc, bool vec) {
+    if (row >= M) return;
+    double *crow = Cm + (int64_t)row * ldc;
+    if (vec && col + 3 < N) {
+        double o[4];
+        if (beta != 0.0) {
+            double c[4];
+            ldg_v4(crow + col, c[0], c[1], c[2], c[3]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) o[e] = fma(alpha, v[e], beta * c[e]);
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) o[e] = alpha * v[e];
+        }
+        stg_v4(crow + col, o[0], o[1], o[2], o[3]);
+    } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            if (col + e < N) {
+                const double o = (beta != 0.0) ? fma(alpha, v[e], beta * crow[col + e]) : alpha * v[e];
+                crow[col + e] = o;
+            }
+        }
+    }
+}
+
 template <class C>
 __device__ __forceinline__ void epilogue(const double (&acc)[C::MB][C::NP][2][2], int row0, int col0, int lane,
                                          int M, int N, double alpha, double beta, double *__restrict__ Cm,
@@ -171,34 +199,10 @@ __device__ __forceinline__ void epilogue(const double (&acc)[C::MB][C::NP][2][2]
     const int g = lane >> 2, t = lane & 3;
 #pragma unroll
     for (int mb = 0; mb < C::MB; ++mb) {
-        const int row = row0 + mb * 8 + g;
-        if (row >= M) continue;
-        double *crow = Cm + (int64_t)row * ldc;
 #pragma unroll
         for (int np = 0; np < C::NP; ++np) {
-            const int col = col0 + np * 16 + 4 * t;
-            double v[4] = {acc[mb][np][0][0], acc[mb][np][1][0], acc[mb][np][0][1], acc[mb][np][1][1]};
-            if (vec && col + 3 < N) {
-                double o[4];
-                if (beta != 0.0) {
-                    double c[4];
-                    ldg_v4(crow + col, c[0], c[1], c[2], c[3]);
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) o[e] = fma(alpha, v[e], beta * c[e]);
-                } else {
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) o[e] = alpha * v[e];
-                }
-                stg_v4(crow + col, o[0], o[1], o[2], o[3]);
-            } else {
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    if (col + e < N) {
-                        const double o = (beta != 0.0) ? fma(alpha, v[e], beta * crow[col + e]) : alpha * v[e];
-                        crow[col + e] = o;
-                    }
-                }
-            }
+            const double v[4] = {acc[mb][np][0][0], acc[mb][np][1][0], acc[mb][np][0][1], acc[mb][np][1][1]};
+            epilogue_quad(v, row0 + mb * 8 + g, col0 + np * 16 + 4 * t, M, N, alpha, beta, Cm, ldc, vec);
         }
     }
 }
@@ -581,6 +585,188 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
                         ldc, vec != 0);
         ++tile;
         kb = 0;
+    }
+}
+
+// ------------------------------------------------------------------------------
+// Hybrid schedule (row a5, large shapes).  The T tiles split into W*G data-parallel tiles
+// (W = floor(T/G) full waves of G = SMs x resident CTAs; run by the plain XP kernel, one
+// tile per CTA) and a tail of T - W*G < G tiles, which alone would leave most SMs idle in
+// a partial last wave.  The tail's Ut = tail*KT k-steps are shared stream-K style by gsk
+// CTAs of dgemm_sktail_kernel (gsk >= tail, so a CTA's range spans at most two tiles).  A
+// tail segment that is a whole tile gets the plain epilogue; any other stores its raw
+// partial to workspace slot 2g+j (j = segment 0/1 of CTA g), and
+// dgemm_hybrid_fixup_kernel sums each cut tile's partials in k order and runs the epilogue.
+// (A persistent kernel that also ran the full waves was measured 1-3 % slower: CTAs that
+// pick up tiles at different times fall out of k-lockstep, and the L2 working set of a
+// wave -- shared A/B k-slices -- grows; DRAM reads rose from 6.4 to 7.5 GB at 8192^3.)
+struct HybArgs {
+    int tile0;      // first tail tile (= W*G)
+    int gsk;        // CTAs sharing the tail
+    double *ws;     // [2*gsk][E/4][warps][32][4] partials
+};
+
+template <class C>
+__global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
+    dgemm_sktail_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
+                        int N, int K, double alpha, double beta, double *__restrict__ Cm, int64_t ldc, int vec,
+                        int group_m, HybArgs hy) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t *base_ptr = smem_raw + (base - raw);
+    uint64_t *full = reinterpret_cast<uint64_t *>(base_ptr + C::STAGES * C::STAGE_BYTES);
+    uint64_t *empty = full + C::STAGES;
+
+    const int tiles_m = (M + C::BM - 1) / C::BM, tiles_n = (N + C::BN - 1) / C::BN;
+    const int KT = (K + C::BK - 1) / C::BK;
+    const int g = blockIdx.x;
+    // this CTA's range [u0, u1) of tail k-steps (host: tiles * KT < 2^31)
+    const int64_t Ut = (int64_t)(tiles_m * tiles_n - hy.tile0) * KT;
+    const int u0 = (int)((int64_t)g * Ut / hy.gsk), u1 = (int)((int64_t)(g + 1) * Ut / hy.gsk);
+    if (u1 <= u0) return;
+    const int ta = u0 / KT;                       // first (tail-local) tile
+    const int nseg = (u1 - 1) / KT - ta + 1;      // 1 or 2
+    const int total = u1 - u0;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool producer = (threadIdx.x == 0);
+    uint64_t pol = 0;
+
+    // producer cursor: k-step, segment end, tile origin
+    int pc_k = u0 - ta * KT, pc_ke = (u1 - ta * KT) < KT ? (u1 - ta * KT) : KT, pc_m0 = 0, pc_n0 = 0;
+    auto pc_tile = [&](int t) {
+        int tm, tn;
+        tile_coords(hy.tile0 + t, tiles_m, tiles_n, group_m, tm, tn);
+        pc_m0 = tm * C::BM;
+        pc_n0 = tn * C::BN;
+    };
+    auto issue_next = [&](int slot) {
+        tma_issue_stage<C>(base_ptr + slot * C::STAGE_BYTES, &tmA, &tmB, &full[slot], pc_m0, pc_n0, pc_k, pol);
+        if (++pc_k == pc_ke && nseg == 2) {   // second segment: tile ta+1 from k-step 0
+            pc_k = 0;
+            pc_ke = u1 - (ta + 1) * KT;
+            pc_tile(ta + 1);
+        }
+    };
+
+    if (producer) {
+#pragma unroll
+        for (int s = 0; s < C::STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], C::CONSUMER_WARPS);
+        }
+        fence_mbar_init();
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+        pol = l2_policy_evict_normal();
+        pc_tile(ta);
+        for (int s = 0; s < C::STAGES && s < total; ++s) issue_next(s);
+    }
+    __syncthreads();
+
+    const int warp_m = warp / C::WARPS_N, warp_n = warp % C::WARPS_N;
+    const FragOffsets<C> fo(warp_m, warp_n, lane);
+    constexpr int H = 2 * C::KG;
+    double acc[C::MB][C::NP][2][2];
+    int it = 0;
+    int stage = 0, phase = 0;
+    for (int j = 0; j < nseg; ++j) {
+        const int t = ta + j;
+        const int kb = j == 0 ? u0 - t * KT : 0;
+        const int ke = (u1 - t * KT) < KT ? (u1 - t * KT) : KT;
+        const int NK = ke - kb;
+#pragma unroll
+        for (int mb = 0; mb < C::MB; ++mb)
+#pragma unroll
+            for (int np = 0; np < C::NP; ++np)
+#pragma unroll
+                for (int jj = 0; jj < 2; ++jj) acc[mb][np][jj][0] = acc[mb][np][jj][1] = 0.0;
+        Frag<C> f[2];
+        mbar_wait(&full[stage], (uint32_t)phase);
+        load_half<C>(base + stage * C::STAGE_BYTES, base + stage * C::STAGE_BYTES + C::A_BYTES, 0, fo, f[0]);
+        for (int i = 0; i < NK; ++i, ++it) {
+            if (producer && it > 0 && it - 1 + C::STAGES < total) {
+                const int sp = stage == 0 ? C::STAGES - 1 : stage - 1;   // slot released at it-1
+                const int pp = stage == 0 ? phase ^ 1 : phase;
+                mbar_wait(&empty[sp], (uint32_t)pp);
+                issue_next(sp);
+            }
+            const uint32_t sA = base + stage * C::STAGE_BYTES;
+            const int s1 = stage + 1 == C::STAGES ? 0 : stage + 1;
+            const int p1 = stage + 1 == C::STAGES ? phase ^ 1 : phase;
+#pragma unroll
+            for (int h = 0; h < H; ++h) {
+                if (h + 1 < H) {
+                    load_half<C>(sA, sA + C::A_BYTES, h + 1, fo, f[(h + 1) & 1]);
+                } else if (i + 1 < NK) {   // cross-stage prefetch inside the segment
+                    mbar_wait(&full[s1], (uint32_t)p1);
+                    const uint32_t sA1 = base + s1 * C::STAGE_BYTES;
+                    load_half<C>(sA1, sA1 + C::A_BYTES, 0, fo, f[0]);
+                }
+                mma_half<C>(f[h & 1], acc);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            stage = s1;
+            phase = p1;
+        }
+        if (kb == 0 && ke == KT) {   // the whole tile: plain epilogue
+            int tm, tn;
+            tile_coords(hy.tile0 + t, tiles_m, tiles_n, group_m, tm, tn);
+            epilogue<C>(acc, tm * C::BM + warp_m * C::WM, tn * C::BN + warp_n * C::WN, lane, M, N, alpha, beta, Cm,
+                        ldc, vec != 0);
+        } else {
+            constexpr int Q = C::E / 4;
+            constexpr int64_t QSTRIDE = (int64_t)C::CONSUMER_WARPS * 32 * 4;
+            double *mine = partial_slot<C>(hy.ws, 2 * g + j, warp, lane);
+            const double *flat = &acc[0][0][0][0];
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+                stg_v4(mine + q * QSTRIDE, flat[4 * q], flat[4 * q + 1], flat[4 * q + 2], flat[4 * q + 3]);
+        }
+    }
+}
+
+// Tail fix-up: one CTA per tail tile; a tile cut between CTAs gets the sum of its
+// partials in k order (CTA jlo's segment first), then the plain epilogue.
+template <class C>
+__global__ void __launch_bounds__(C::CONSUMER_THREADS, 1)
+    dgemm_hybrid_fixup_kernel(int M, int N, int K, double alpha, double beta, double *__restrict__ Cm, int64_t ldc,
+                              int vec, int group_m, int tdp, int gsk, const double *__restrict__ ws) {
+    const int tiles_m = (M + C::BM - 1) / C::BM, tiles_n = (N + C::BN - 1) / C::BN;
+    const int KT = (K + C::BK - 1) / C::BK;
+    const int64_t Ut = (int64_t)(tiles_m * tiles_n - tdp) * KT;
+    const int b = blockIdx.x;
+    const int64_t t0 = (int64_t)b * KT;
+    const int jlo = (int)sk_count_le(t0, Ut, gsk) - 1;             // CTA holding k-step t0
+    const int jhi = (int)sk_count_le(t0 + KT - 1, Ut, gsk) - 1;    // CTA holding the last k-step
+    if (jlo == jhi) return;   // one CTA covered the whole tile: epilogue already done
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp_m = warp / C::WARPS_N, warp_n = warp % C::WARPS_N;
+    constexpr int64_t QSTRIDE = (int64_t)C::CONSUMER_WARPS * 32 * 4;
+    int tm, tn;
+    tile_coords(tdp + b, tiles_m, tiles_n, group_m, tm, tn);
+    const int row0 = tm * C::BM + warp_m * C::WM + (lane >> 2);
+    const int col0 = tn * C::BN + warp_n * C::WN + 4 * (lane & 3);
+    // quad q = mb * NP + np holds flat accumulators 4q..4q+3 = acc[mb][np][j][i] (j major)
+#pragma unroll 1
+    for (int q = 0; q < C::MB * C::NP; ++q) {
+        double x[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int j = jlo; j <= jhi; ++j) {
+            const int slot = 2 * j + (sk_bound(j, Ut, gsk) >= t0 ? 0 : 1);
+            const double *src = partial_slot<C>(const_cast<double *>(ws), slot, warp, lane) + q * QSTRIDE;
+            double v0, v1, v2, v3;
+            asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];\n"
+                         : "=d"(v0), "=d"(v1), "=d"(v2), "=d"(v3)
+                         : "l"(src));
+            x[0] += v0;
+            x[1] += v1;
+            x[2] += v2;
+            x[3] += v3;
+        }
+        const int mb = q / C::NP, np = q - mb * C::NP;
+        const double v[4] = {x[0], x[2], x[1], x[3]};   // (j,i) = (0,0), (1,0), (0,1), (1,1)
+        epilogue_quad(v, row0 + mb * 8, col0 + np * 16, M, N, alpha, beta, Cm, ldc, vec != 0);
     }
 }
 

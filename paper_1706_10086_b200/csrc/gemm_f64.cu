@@ -241,6 +241,7 @@ struct Cand {
 };
 static const Cand k_tma_cands[] = {
     {"tma_256x64x16_w64x32_s4_xp", 0.981},     {"tma_128x128x16_w64x32_s4_xp", 0.979},
+    {"tma_256x64x16_w64x32_s4_hybrid", 0.981},
     {"tma_64x128x16_w32x64_s4", 0.972},
     {"tma_128x128x16_w32x32_s4", 0.965},       {"tma_64x64x16_w32x16_s6", 0.952},
     {"tma_64x64x16_w32x16_s6_splitk", 0.950},  {"tma_128x64x16_w32x16_s6_splitk", 0.945},
@@ -292,7 +293,7 @@ static Choice choose(int64_t M, int64_t N, int64_t K, bool tma, bool single_pass
         std::lock_guard<std::mutex> lk(g_plan_mu);
         auto pin = g_pinned.find(PlanKey{0, M, N, K, tma});
         if (pin != g_pinned.end() &&
-            (!single_pass || (g_cfgs[pin->second.id].d.split_k != -1 && pin->second.splits == 1)))
+            (!single_pass || (g_cfgs[pin->second.id].d.split_k >= 0 && pin->second.splits == 1)))
             return pin->second;
         auto it = g_plans.find(key);
         if (it != g_plans.end()) return it->second;
@@ -324,6 +325,23 @@ static Choice choose_uncached(int64_t M, int64_t N, int64_t K, bool tma, bool si
         const gemm_cfg_desc &d = g_cfgs[id].d;
         const int64_t KT = (K + d.bk - 1) / d.bk;
         if (single_pass && d.split_k != 1) continue;
+        if (d.split_k == -2) {   // hybrid: W full waves + the tail's k-steps spread over gsk CTAs
+            const int64_t tiles = ((M + d.bm - 1) / d.bm) * ((N + d.bn - 1) / d.bn);
+            const int64_t G = (int64_t)sms * occ;
+            const int64_t W = tiles / G, tail = tiles - W * G;
+            double ks = (double)W * (double)(KT + 4);
+            if (tail > 0) {   // + pipeline fill, partial store, fix-up and two launch gaps
+                const int64_t gsk = std::min<int64_t>(G, std::max<int64_t>(tail, tail * KT / 16));
+                ks += (double)((tail * KT + gsk - 1) / gsk) + 12.0;
+            }
+            const double t = ks * occ * d.bm * d.bn * (d.bk / 16.0) / c.eff;
+            if (t < best_t * 0.999) {
+                best_t = t;
+                best.id = id;
+                best.splits = 1;
+            }
+            continue;
+        }
         if (d.split_k == -1) {   // stream-K: every CTA gets ceil(U/G) k-steps, no partial waves
             const int64_t tiles = ((M + d.bm - 1) / d.bm) * ((N + d.bn - 1) / d.bn);
             const int64_t G = std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * occ, tiles * KT));
@@ -562,7 +580,7 @@ int gemm_impl(int64_t M, int64_t N, int64_t K, double alpha, const double *A, in
     const gemm_cfg_desc &d = g_cfgs[id].d;
     if (force_splits < 0) return set_error(GEMM_ERR_ARG, "splits=%d must be >= 0", force_splits);
     if (cfg_id >= 0 && d.split_k == 0) splits = force_splits > 0 ? force_splits : auto_splits(id, M, N, K);
-    if (d.split_k == -1) splits = 1;   // stream-K: the work split is fixed by the grid, not by S
+    if (d.split_k < 0) splits = 1;   // stream-K / hybrid: the work split is fixed by the grid, not by S
     if (force_splits > 1 && d.split_k != 0)
         return set_error(GEMM_ERR_UNSUPPORTED, "cfg %s has no split-K (use a *_splitk configuration)", g_cfgs[id].name);
     if (splits > 4096) return set_error(GEMM_ERR_ARG, "splits=%d > 4096", splits);

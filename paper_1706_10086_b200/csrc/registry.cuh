@@ -1,5 +1,6 @@
 // registry.cuh -- configuration table entries and the launch templates.
 #pragma once
+#include <algorithm>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -59,6 +60,7 @@ static int launch_generic(const LaunchArgs &a, cudaStream_t st) {
 // Stream-K launch: grid = min(U, SMs x resident CTAs); workspace = 2 partial slots per CTA.
 int streamk_workspace(cudaStream_t st, size_t slot_doubles, int grid, size_t tiles, double **ws, int **ctr);
 int streamk_grid(const void *kernel, int threads, int smem, int64_t units);
+constexpr int64_t kHybMinSteps = 16;   // hybrid tail: at least this many k-steps per stream-K CTA
 
 template <class C>
 static int launch_streamk(const LaunchArgs &a, cudaStream_t st) {
@@ -82,7 +84,56 @@ static int launch_streamk(const LaunchArgs &a, cudaStream_t st) {
     return cuda_check(cudaGetLastError(), "dgemm_streamk_kernel launch");
 }
 
-#define DG_SK(BM, BN, BK, WM, WN, ST)                                                                        \
+// Hybrid launch: the W full data-parallel waves as one plain XP launch (grid = W*G tiles),
+// then the tail's k-steps over gsk stream-K CTAs, then the fix-up of the cut tail tiles.
+template <class C>
+static int launch_hybrid(const LaunchArgs &a, cudaStream_t st) {
+    const void *dp_kernel = (const void *)dgemm_tma_kernel<C, false, true>;
+    const void *sk_kernel = (const void *)dgemm_sktail_kernel<C>;
+    int rc = cuda_check(cudaFuncSetAttribute(dp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES),
+                        "cudaFuncSetAttribute(hybrid data-parallel kernel)");
+    if (rc) return rc;
+    CUtensorMap ta, tb;
+    rc = make_tmap(&ta, a.A, a.M, a.K, a.lda, C::BM);
+    if (rc) return rc;
+    rc = make_tmap(&tb, a.B, a.K, a.N, a.ldb, 16);
+    if (rc) return rc;
+    const int64_t tiles = ((int64_t)a.M + C::BM - 1) / C::BM * (((int64_t)a.N + C::BN - 1) / C::BN);
+    const int64_t KT = ((int64_t)a.K + C::BK - 1) / C::BK;
+    if (tiles * KT > 0x7FFFFFFF) return set_error(GEMM_ERR_UNSUPPORTED, "hybrid needs tiles*k-steps < 2^31");
+    const int G = streamk_grid(dp_kernel, C::CONSUMER_THREADS, C::SMEM_BYTES, 1LL << 40);
+    if (G <= 0) return set_error(GEMM_ERR_CUDA, "hybrid occupancy query failed");
+    const int64_t tdp = tiles / G * G, tail = tiles - tdp;
+    if (tdp > 0) {
+        SplitArgs none{1, nullptr, nullptr};
+        dgemm_tma_kernel<C, false, true><<<(unsigned)tdp, C::CONSUMER_THREADS, C::SMEM_BYTES, st>>>(
+            ta, tb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec, a.group_m, none);
+        rc = cuda_check(cudaGetLastError(), "hybrid data-parallel launch");
+        if (rc || tail == 0) return rc;
+    }
+    HybArgs hy{(int)tdp, 0, nullptr};
+    const int64_t Ut = tail * KT;
+    hy.gsk = (int)std::min<int64_t>(G, std::max<int64_t>(tail, Ut / kHybMinSteps));
+    int *ctr = nullptr;
+    rc = streamk_workspace(st, (size_t)C::BM * C::BN, hy.gsk, 0, &hy.ws, &ctr);
+    if (rc) return rc;
+    dgemm_sktail_kernel<C><<<hy.gsk, C::CONSUMER_THREADS, C::SMEM_BYTES, st>>>(
+        ta, tb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec, a.group_m, hy);
+    rc = cuda_check(cudaGetLastError(), "dgemm_sktail_kernel launch");
+    if (rc || ((int64_t)hy.gsk == tail && Ut % hy.gsk == 0)) return rc;   // every tail CTA had a whole tile
+    dgemm_hybrid_fixup_kernel<C><<<(unsigned)tail, C::CONSUMER_THREADS, 0, st>>>(
+        a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec, a.group_m, (int)tdp, hy.gsk, hy.ws);
+    return cuda_check(cudaGetLastError(), "dgemm_hybrid_fixup_kernel launch");
+}
+
+#define DG_HYB(BM, BN, BK, WM, WN, ST)                                                                       \
+    CfgEntry{"tma_" #BM "x" #BN "x" #BK "_w" #WM "x" #WN "_s" #ST "_hybrid",                                  \
+             gemm_cfg_desc{BM, BN, BK, WM, WN, ST, Cfg<BM, BN, BK, WM, WN, ST>::CONSUMER_THREADS,              \
+                           (int)Cfg<BM, BN, BK, WM, WN, ST>::SMEM_BYTES, 1, -2, 0},                           \
+             (const void *)dgemm_sktail_kernel<Cfg<BM, BN, BK, WM, WN, ST>>,                                  \
+             launch_hybrid<Cfg<BM, BN, BK, WM, WN, ST>>}
+
+#define DG_SK(BM, BN, BK, WM, WN, ST)                                                                     \
     CfgEntry{"tma_" #BM "x" #BN "x" #BK "_w" #WM "x" #WN "_s" #ST "_streamk",                                 \
              gemm_cfg_desc{BM, BN, BK, WM, WN, ST, Cfg<BM, BN, BK, WM, WN, ST>::CONSUMER_THREADS,              \
                            (int)Cfg<BM, BN, BK, WM, WN, ST>::SMEM_BYTES, 1, -1, 0},                           \

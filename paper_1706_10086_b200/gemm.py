@@ -262,6 +262,28 @@ def plan(M, N, K, A_ptr=0, lda=None, B_ptr=0, ldb=None) -> tuple:
     return cid.value, sp.value
 
 
+HYB_MIN_STEPS = 16   # registry.cuh kHybMinSteps
+
+
+def launches_per_call(cfg: int, M: int, N: int, K: int, sms: int = 148) -> int:
+    """Kernels one gemm call with configuration `cfg` launches (alpha != 0, K > 0): 1 for the
+    one-kernel schedules (plain, split-K with in-kernel reduction, stream-K); the hybrid
+    (split_k = -2) launches the data-parallel waves, the stream-K tail and the tail fix-up,
+    each only when needed (mirrors launch_hybrid in csrc/registry.cuh; one CTA per SM)."""
+    d = cfg_info(cfg)
+    if d["split_k"] != -2:
+        return 1
+    tiles = -(-M // d["bm"]) * -(-N // d["bn"])
+    kt = -(-K // d["bk"])
+    tdp = tiles // sms * sms
+    tail = tiles - tdp
+    if tail == 0:
+        return 1
+    gsk = min(sms, max(tail, tail * kt // HYB_MIN_STEPS))
+    fixup = not (gsk == tail and (tail * kt) % gsk == 0)
+    return (1 if tdp > 0 else 0) + 1 + (1 if fixup else 0)
+
+
 def plan_set(M, N, K, tma: bool, cfg: int, splits: int = 1):
     """Pin the plan used for (M, N, K, TMA-eligible) on the current device."""
     _check(_lib.gemm_plan_set(M, N, K, int(bool(tma)), int(cfg), int(splits)))

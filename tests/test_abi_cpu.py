@@ -73,9 +73,12 @@ def test_sass_gemm_kernels_use_dmma_tma_and_no_spills(sass):
     gemm = {k: v for k, v in funcs.items() if "dgemm_" in k}
     assert gemm, "no GEMM kernels found"
     for name, body in gemm.items():
-        assert "DMMA.8x8x4" in body, name
         assert not re.search(r"\b(LDL|STL)\b", body), f"local-memory spill in {name}"
-        if "dgemm_tma_kernel" in name:
+        if "fixup" in name:          # hybrid tail reduction: loads partials, no MMA
+            assert "STG.E.ENL2.256" in body, name
+            continue
+        assert "DMMA.8x8x4" in body, name
+        if "dgemm_tma_kernel" in name or "dgemm_sktail_kernel" in name:
             assert "UTMALDG" in body, name
             assert "STG.E.ENL2.256" in body, name
         if "dgemm_generic_kernel" in name:
@@ -193,3 +196,16 @@ def test_sass_f32_kernels_use_tcgen05(sass):
         assert "LDTM" in body, name
         assert "UTMALDG" in body, name
         assert not re.search(r"\b(LDL|STL)\b", body), name
+
+
+def test_hybrid_launch_count(G):
+    """Host mirror of launch_hybrid: data-parallel waves, stream-K tail, fix-up when needed."""
+    hyb = G.cfg_id("tma_256x64x16_w64x32_s4_hybrid")
+    xp = G.cfg_id("tma_256x64x16_w64x32_s4_xp")
+    assert G.launches_per_call(xp, 16384, 16384, 16384) == 1
+    assert G.launches_per_call(hyb, 1024, 2368, 64) == 1          # 148 tiles: one full wave, no tail
+    assert G.launches_per_call(hyb, 1024, 2496, 32) == 2          # tail CTAs own whole tiles: no fix-up
+    assert G.launches_per_call(hyb, 16384, 16384, 16384) == 3     # 110 waves + 104-tile tail
+    assert G.launches_per_call(hyb, 300, 200, 2000) == 2          # no full wave: tail + fix-up
+    info = G.cfg_info(hyb)
+    assert info["split_k"] == -2 and info["tma"] == 1

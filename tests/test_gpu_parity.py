@@ -130,9 +130,9 @@ def test_all_cfgs_bitwise_identical_and_deterministic(cuda_lib):
     """Every configuration sums each entry in the same order (16-deep k-groups ascending,
     same k-permutation, same DMMA chain) -> identical bits; and runs repeat bitwise."""
     A, B, C0 = synth.problem(334, 290, 778, seed=3)
-    # split-K configurations with one slice run the same chain as the others; stream-K
-    # cuts tiles between CTAs (a different association) and is checked separately
-    ids = [c["id"] for c in cuda_lib.cfgs() if c["split_k"] != -1]
+    # split-K configurations with one slice run the same chain as the others; stream-K and
+    # the hybrid cut tiles between CTAs (a different association) and are checked separately
+    ids = [c["id"] for c in cuda_lib.cfgs() if c["split_k"] >= 0]
     outs = [run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=c, splits=1) for c in ids]
     for c, o in zip(ids, outs):
         assert np.array_equal(o, outs[0]), cuda_lib.cfg_name(c)
@@ -147,7 +147,7 @@ def split_cfgs(G):
 
 
 def streamk_cfgs(G):
-    return [c["id"] for c in G.cfgs() if c["split_k"] == -1]
+    return [c["id"] for c in G.cfgs() if c["split_k"] < 0]   # stream-K and hybrid
 
 
 @pytest.mark.parametrize("shape", [(70, 90, 1000), (256, 256, 256), (129, 200, 777), (64, 64, 16), (31, 33, 2000)],
@@ -557,3 +557,46 @@ def test_cuda_graph_capture_and_replay(cuda_lib):
     eager = run_gpu(cuda_lib, A, B, C0, 1.0, 0.0)
     for o in outs:
         assert np.array_equal(o.cpu().numpy(), eager)
+
+
+# ---------------------------------------------------------------- hybrid (row a5)
+HYBRID_SHAPES = [
+    (1024, 2368, 64),     # T = 148 tiles = one full wave, no tail
+    (1024, 2496, 32),     # tail of 8 tiles, KT = 2 < 16: one whole tile per tail CTA, no fix-up
+    (1000, 2500, 1000),   # W = 1 + 12 cut tail tiles, ragged M / N / K
+    (300, 200, 2000),     # W = 0: pure stream-K over 8 tiles
+    (256, 64, 16),        # one tile, one k-step
+    (520, 130, 778),
+]
+
+
+@pytest.mark.parametrize("shape", HYBRID_SHAPES, ids=lambda s: "x".join(map(str, s)))
+def test_hybrid_within_bound_deterministic(cuda_lib, shape):
+    """Persistent data-parallel waves + stream-K tail + fix-up: every wave/tail layout."""
+    M, N, K = shape
+    A, B, C0 = synth.problem(M, N, K, seed=M + K)
+    hyb = cuda_lib.cfg_id("tma_256x64x16_w64x32_s4_hybrid")
+    C = run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=hyb)
+    check_vs_oracle(C, A, B, C0, 1.5, 0.5)
+    assert np.array_equal(C, run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=hyb))
+    # tiles not cut by the tail carry the plain one-pass chain: identical to the XP kernel
+    xp = run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=cuda_lib.cfg_id("tma_256x64x16_w64x32_s4_xp"))
+    G_ = torch.cuda.get_device_properties(0).multi_processor_count
+    tn = (N + 63) // 64
+    T = ((M + 255) // 256) * tn
+    full = T - T % G_ if T >= G_ else 0
+    rows_done = np.zeros((M, N), dtype=bool)
+    for bid in range(full):          # grouped raster, group_m = 8 (tile_coords)
+        per = 8 * tn
+        grp, r = divmod(bid, per)
+        gs = min(8, (M + 255) // 256 - grp * 8)
+        tm, tnn = grp * 8 + r % gs, r // gs
+        rows_done[tm * 256:(tm + 1) * 256, tnn * 64:(tnn + 1) * 64] = True
+    assert np.array_equal(C[rows_done], xp[rows_done])
+
+
+def test_hybrid_exact_regime_bitwise(cuda_lib):
+    A, B, C0 = synth.problem(1000, 2500, 1000, mode="dyadic", seed=12)
+    ref = oracle.dgemm(1.5, A, B, 0.5, C0)
+    hyb = cuda_lib.cfg_id("tma_256x64x16_w64x32_s4_hybrid")
+    assert np.array_equal(run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=hyb), ref)
