@@ -36,6 +36,16 @@ def main():
         c32 = torch.zeros((M, N), dtype=torch.float32, device="cuda")
         G.gemm_f32(a32, b32, c32, 1.5, 0.5)  # 3xTF32 tcgen05 path
         n += 2
+    # hybrid schedule with a full wave, a cut stream-K tail and the fix-up kernel
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    M, N, K = 1000, 64 * (sms // 4 + 3), 1000
+    A = torch.rand((M, K), dtype=torch.float64, device="cuda")
+    B = torch.rand((K, N), dtype=torch.float64, device="cuda")
+    C = torch.zeros((M, N), dtype=torch.float64, device="cuda")
+    hyb = G.cfg_id("tma_256x64x16_w64x32_s4_hybrid")
+    assert G.launches_per_call(hyb, M, N, K, sms) == 3
+    G.gemm(A, B, C, 1.0, 0.0, cfg=hyb)
+    n += 1
     # repack path: large problem with odd leading dimensions
     M, N, K = 1200, 1201, 1501
     A = torch.rand((M, K), dtype=torch.float64, device="cuda")
