@@ -195,12 +195,15 @@ def small(a):
 
 
 def ncu_pass(a):
+    """One call per configuration (ncu --metrics over the dgemm_ kernels); prints
+    "cfg_id name launches" so a joiner can group the captured kernels per configuration."""
     P = Problem(a.n, a.n, a.n)
     P.reset_c()
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
     for info in G.cfgs():
         G.gemm(P.A, P.B, P.C, a.alpha, a.beta, cfg=info["id"])
         torch.cuda.synchronize()
-        print(info["id"], info["name"], flush=True)
+        print(info["id"], info["name"], G.launches_per_call(info["id"], a.n, a.n, a.n, sms), flush=True)
 
 
 def main():
