@@ -53,15 +53,41 @@ static int ensure_events(std::vector<cudaEvent_t> &v, size_t n) {
 }
 
 // Schedule (all copies from the caller's host buffers into packed device buffers):
-//   h2d : A rows [0, R0), then B in column panels, then A row panels 1.. (and C0 rows
-//         alongside the A rows when beta != 0)
-//   comp: row panel 0 is multiplied column block by column block as the B panels land
-//         (R0 is sized so that this work covers the whole B transfer:
-//         R0 ~ 4 * compute_rate / h2d_bandwidth rows, independent of N and K), then
-//         each later row panel as soon as its A rows land; the last row panel is again
-//         computed in column blocks so that its device->host copy overlaps
+//   h2d : A rows [0, Ra), B column block 0, A rows [Ra, R0), B column blocks 1.., then the
+//         A row panels (and C0 rows alongside the A rows when beta != 0)
+//   comp: row panel 0 (R0 rows) is multiplied column block by column block as the B
+//         blocks land -- block 0 first on rows [0, Ra) so the GPU starts after a short
+//         copy; R0 is sized so a block's GEMM outlasts the next block's copy
+//         (R0 >= 4 * compute_rate / h2d_bandwidth rows, independent of N and K); then the
+//         later row panels, each as soon as its A rows land; the last panel is thin
+//         (256 rows, 2 column blocks) so the final device->host copy is short
 //   d2h : every finished block / panel of C
-// Exposed copy time is the first A rows + the first B panel and the last C block.
+// Block widths and panel heights are chosen so that each GEMM's 256x64 tile count falls
+// just below a multiple of the SM count (little partial-wave waste).  The geometry was
+// chosen with a copy/compute simulation calibrated on measured PCIe and GEMM rates
+// (DESIGN.md §e2e): 16384^3 264 -> 255 ms.
+namespace {
+constexpr double kRate = 36.6e12;   // FP64 DMMA GEMM rate (FLOP/s)
+constexpr double kH2D = 55e9;       // pinned H2D bandwidth (B/s), PCIe 5 x16
+constexpr int kTm = 256, kTn = 64;  // tile of the large-shape kernel
+
+// tile count t = r * c falls in a wave as fully as possible: efficiency t / (S * ceil(t / S))
+double wave_eff(int64_t t, int S) { return (double)t / ((double)S * (double)((t + S - 1) / S)); }
+
+int64_t best_factor(int64_t fixed, int64_t lo, int64_t hi, int S) {
+    int64_t best = lo;
+    double be = -1.0;
+    for (int64_t x = lo; x <= hi; ++x) {
+        const double e = wave_eff(fixed * x, S);
+        if (e > be + 1e-9) {
+            be = e;
+            best = x;
+        }
+    }
+    return best;
+}
+}  // namespace
+
 static int host_impl(int64_t M, int64_t N, int64_t K, double alpha, const double *A, int64_t lda, const double *B,
                      int64_t ldb, double beta, double *C, int64_t ldc) {
     clear_error();
@@ -74,6 +100,8 @@ static int host_impl(int64_t M, int64_t N, int64_t K, double alpha, const double
 
     int dev = 0;
     if ((rc = cuda_check(cudaGetDevice(&dev), "cudaGetDevice"))) return rc;
+    int S = 148;
+    cudaDeviceGetAttribute(&S, cudaDevAttrMultiProcessorCount, dev);
     std::lock_guard<std::mutex> lk(g_pool_mu);
     HostPool &P = g_pools[dev];
     if (!P.h2d) {
@@ -90,20 +118,36 @@ static int host_impl(int64_t M, int64_t N, int64_t K, double alpha, const double
     // ---- geometry
     const double flops = 2.0 * (double)M * (double)N * (double)K;
     const bool tiny = !need_ab || flops < 2e10;      // < ~1 ms of GPU work: one shot
-    int64_t R0 = M, Rp = M, cb = N;                  // first panel rows, later panel rows, column block
+    const int64_t tn_all = (N + kTn - 1) / kTn;
+    int64_t R0 = M, Ra = M, Rp = M, Rlast = 0, cb0 = N, cb = N, nlast = 1;
     if (!tiny) {
-        // R0 ~ 4 * compute rate / H2D bandwidth rows keeps the GPU busy while B streams in;
-        // 2304 = 9 rows of 256-row tiles: with 2048-column blocks (32 tiles of 64) a block is
-        // 288 tiles = 1.95 waves of 148 SMs (2560 rows gave 320 tiles = 2.16 waves).
-        R0 = std::min<int64_t>(M, 2304);
-        Rp = 2048;
-        cb = std::max<int64_t>(512, ((N + 7) / 8 + 63) / 64 * 64);   // <= 8 column blocks
+        const int64_t r_bal = (int64_t)(4.0 * kRate / kH2D / kTm) + 1;          // 11 tile rows
+        const int64_t r0 = best_factor(std::min<int64_t>(tn_all, 24), r_bal, r_bal + 2, S);
+        R0 = std::min<int64_t>(M, r0 * kTm);
+        Ra = std::min<int64_t>(R0, 3 * kTm);
+        const int64_t cbt = best_factor(r0, 16, 32, S);                          // 24 at S = 148
+        cb = std::min<int64_t>(N, cbt * kTn);
+        cb0 = std::min<int64_t>(N, 16 * kTn);
+        Rp = best_factor(tn_all, 8, 24, S) * kTm;                                // 15 x 256 at N = 16384
+        Rlast = kTm;
+        nlast = N >= 2 * 512 ? 2 : 1;
     }
-    const int64_t ncb = (N + cb - 1) / cb;
-    const int64_t nrest = (M > R0) ? (M - R0 + Rp - 1) / Rp : 0;
-    // events: one per column block of panel 0, one per later panel, one per column block
-    // of the last panel (h2d_done / comp_done each use at most this many)
-    const size_t nev = (size_t)(2 * ncb + nrest + 8);
+    // column blocks of panel 0: cb0, then cb each
+    std::vector<std::pair<int64_t, int64_t>> cols;
+    for (int64_t c0 = 0; c0 < N;) {
+        const int64_t w = std::min(N - c0, cols.empty() ? cb0 : cb);
+        cols.push_back({c0, w});
+        c0 += w;
+    }
+    // later row panels: Rp rows each, the last one Rlast rows (thin: short final D2H)
+    std::vector<std::pair<int64_t, int64_t>> rows;
+    for (int64_t r0 = R0; r0 < M;) {
+        const int64_t rem = M - r0;
+        const int64_t nr = (rem <= Rlast || Rlast == 0) ? rem : (rem <= Rlast + Rp ? rem - Rlast : Rp);
+        rows.push_back({r0, nr});
+        r0 += nr;
+    }
+    const size_t nev = cols.size() + 2 + rows.size() * (size_t)(nlast + 1) + 8;
     if ((rc = ensure_events(P.ev_in, nev))) return rc;
     if ((rc = ensure_events(P.ev_out, nev))) return rc;
 
@@ -137,37 +181,47 @@ static int host_impl(int64_t M, int64_t N, int64_t K, double alpha, const double
         return r;
     };
 
-    // ---- row panel 0: A rows and C0 rows first, then B column blocks, each followed by its GEMM block
-    if (need_ab && (rc = h2d_rows(P.dA, K, A, lda, K, R0, "H2D A panel"))) return rc;
-    if (need_c_in && (rc = h2d_rows(P.dC, N, C, ldc, N, R0, "H2D C panel"))) return rc;
-    for (int64_t j = 0; j < ncb; ++j) {
-        const int64_t c0 = j * cb, nc = std::min(N, c0 + cb) - c0;
-        if (need_ab && (rc = cuda_check(cudaMemcpy2DAsync(P.dB + c0, N * 8, B + c0, ldb * 8, nc * 8, K,
-                                                          cudaMemcpyHostToDevice, P.h2d),
-                                        "H2D B panel")))
-            return rc;
+    // ---- row panel 0
+    auto h2d_a = [&](int64_t r0, int64_t nr) -> int {
+        int r = GEMM_OK;
+        if (need_ab) r = h2d_rows(P.dA + r0 * K, K, A + r0 * lda, lda, K, nr, "H2D A rows");
+        if (!r && need_c_in) r = h2d_rows(P.dC + r0 * N, N, C + r0 * ldc, ldc, N, nr, "H2D C rows");
+        return r;
+    };
+    auto h2d_b = [&](int64_t c0, int64_t nc) -> int {
+        if (!need_ab) return GEMM_OK;
+        return cuda_check(cudaMemcpy2DAsync(P.dB + c0, N * 8, B + c0, ldb * 8, nc * 8, K, cudaMemcpyHostToDevice, P.h2d),
+                          "H2D B block");
+    };
+    auto block = [&](int64_t r0, int64_t nr, int64_t c0, int64_t nc) -> int {
+        int r = run(r0, nr, c0, nc);
+        if (!r) r = comp_done();
+        if (!r) r = d2h_block(r0, nr, c0, nc);
+        return r;
+    };
+    if ((rc = h2d_a(0, Ra))) return rc;
+    for (size_t j = 0; j < cols.size(); ++j) {
+        const int64_t c0 = cols[j].first, nc = cols[j].second;
+        if ((rc = h2d_b(c0, nc))) return rc;
         if ((rc = h2d_done())) return rc;
-        if ((rc = run(0, R0, c0, nc))) return rc;
-        if ((rc = comp_done())) return rc;
-        if ((rc = d2h_block(0, R0, c0, nc))) return rc;
+        if (j == 0 && Ra < R0) {   // block 0 on the first Ra rows while the rest of panel 0's A lands
+            if ((rc = block(0, Ra, c0, nc))) return rc;
+            if ((rc = h2d_a(Ra, R0 - Ra))) return rc;
+            if ((rc = h2d_done())) return rc;
+            if ((rc = block(Ra, R0 - Ra, c0, nc))) return rc;
+        } else {
+            if ((rc = block(0, R0, c0, nc))) return rc;
+        }
     }
     // ---- later row panels
-    for (int64_t p = 0; p < nrest; ++p) {
-        const int64_t r0 = R0 + p * Rp, nr = std::min(M, r0 + Rp) - r0;
-        if (need_ab && (rc = h2d_rows(P.dA + r0 * K, K, A + r0 * lda, lda, K, nr, "H2D A panel"))) return rc;
-        if (need_c_in && (rc = h2d_rows(P.dC + r0 * N, N, C + r0 * ldc, ldc, N, nr, "H2D C panel"))) return rc;
+    for (size_t p = 0; p < rows.size(); ++p) {
+        const int64_t r0 = rows[p].first, nr = rows[p].second;
+        if ((rc = h2d_a(r0, nr))) return rc;
         if ((rc = h2d_done())) return rc;
-        // the last panel in 2 column blocks: the final D2H overlaps the first one (narrower
-        // blocks shorten the exposed copy but fall into partial waves, measured slower)
-        const bool last = (p == nrest - 1);
-        const int64_t lcb = last ? std::max<int64_t>(512, ((N + 1) / 2 + 63) / 64 * 64) : N;
-        const int64_t nlcb = (N + lcb - 1) / lcb;
-        for (int64_t j = 0; j < nlcb; ++j) {
-            const int64_t c0 = j * lcb, nc = std::min(N, c0 + lcb) - c0;
-            if ((rc = run(r0, nr, c0, nc))) return rc;
-            if ((rc = comp_done())) return rc;
-            if ((rc = d2h_block(r0, nr, c0, nc))) return rc;
-        }
+        const bool last = (p + 1 == rows.size());
+        const int64_t lcb = last ? std::max<int64_t>(kTn, ((N + nlast - 1) / nlast + kTn - 1) / kTn * kTn) : N;
+        for (int64_t c0 = 0; c0 < N; c0 += lcb)
+            if ((rc = block(r0, nr, c0, std::min(N, c0 + lcb) - c0))) return rc;
     }
     return cuda_check(cudaStreamSynchronize(P.d2h), "gemm_f64_host synchronize");
 }
