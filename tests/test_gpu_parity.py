@@ -600,3 +600,44 @@ def test_hybrid_exact_regime_bitwise(cuda_lib):
     ref = oracle.dgemm(1.5, A, B, 0.5, C0)
     hyb = cuda_lib.cfg_id("tma_256x64x16_w64x32_s4_hybrid")
     assert np.array_equal(run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=hyb), ref)
+
+
+def _tile_coords(bid, tiles_m, tiles_n, group_m=8):
+    per = group_m * tiles_n
+    grp, r = divmod(bid, per)
+    gs = min(group_m, tiles_m - grp * group_m)
+    return grp * group_m + r % gs, r // gs
+
+
+@pytest.mark.parametrize("shape", [(16384, 4096, 4096), (7168, 7168, 7168)], ids=lambda s: "x".join(map(str, s)))
+def test_hybrid_plan_full_size_tail_rows(cuda_lib, shape):
+    """Full-size shapes the product runs with the hybrid schedule (config-4 2-GPU shard,
+    the f1 grid): rows through the stream-K tail tiles (cut between CTAs, finished by the
+    fix-up kernel) and through data-parallel tiles, checked against the oracle."""
+    M, N, K = shape
+    dA = torch.empty((M, K), dtype=torch.float64, device="cuda")
+    dB = torch.empty((K, N), dtype=torch.float64, device="cuda")
+    dC = torch.empty((M, N), dtype=torch.float64, device="cuda")
+    cid, _ = cuda_lib.plan(M, N, K, dA.data_ptr(), K, dB.data_ptr(), N)
+    assert cuda_lib.cfg_name(cid).endswith("_hybrid"), cuda_lib.cfg_name(cid)
+    cuda_lib.fill(dA, "uniform", 1706, 0)
+    cuda_lib.fill(dB, "uniform", 1706, 1)
+    cuda_lib.fill(dC, "uniform", 1706, 2)
+    cuda_lib.gemm(dA, dB, dC, 1.5, 0.5)
+    torch.cuda.synchronize()
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    tm_n, tn_n = (M + 255) // 256, (N + 63) // 64
+    T = tm_n * tn_n
+    tail = list(range(T - T % sms, T))
+    assert tail, "shape has no tail"
+    tail_rows = sorted({_tile_coords(b, tm_n, tn_n)[0] * 256 + o for b in tail[::max(1, len(tail) // 3)]
+                        for o in (0, 255)})
+    rows = sorted(set(tail_rows) | {0, M // 3})
+    B = synth.matrix("uniform", 1706, 1, K, N)
+    A_r = np.vstack([synth.matrix("uniform", 1706, 0, M, K, row0=r, nrows=1) for r in rows])
+    C0_r = np.vstack([synth.matrix("uniform", 1706, 2, M, N, row0=r, nrows=1) for r in rows])
+    ref, mag = oracle.dgemm(1.5, A_r, B, 0.5, C0_r, want_mag=True)
+    res = oracle.check(dC[torch.tensor(rows, device="cuda")].cpu().numpy(), ref, oracle.bound(K, 1.5, 0.5, mag, C0_r))
+    assert res.ok, f"rows {rows}: {res}"
+    del dA, dB, dC
+    torch.cuda.empty_cache()
