@@ -121,7 +121,8 @@ static int launch_hybrid(const LaunchArgs &a, cudaStream_t st) {
         ta, tb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec, a.group_m, hy);
     rc = cuda_check(cudaGetLastError(), "dgemm_sktail_kernel launch");
     if (rc || ((int64_t)hy.gsk == tail && Ut % hy.gsk == 0)) return rc;   // every tail CTA had a whole tile
-    dgemm_hybrid_fixup_kernel<C><<<(unsigned)tail, C::CONSUMER_THREADS, 0, st>>>(
+    static_assert((C::MB * C::NP) % kFixQ == 0, "fix-up quad split");
+    dgemm_hybrid_fixup_kernel<C><<<dim3((unsigned)tail, C::MB * C::NP / kFixQ), C::CONSUMER_THREADS, 0, st>>>(
         a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec, a.group_m, (int)tdp, hy.gsk, hy.ws);
     return cuda_check(cudaGetLastError(), "dgemm_hybrid_fixup_kernel launch");
 }
