@@ -54,20 +54,29 @@ def select(results, tol: float = TIE_TOL):
     return tied[0]
 
 
-def _time(fn, reps: int, warm_s: float = 0.2):
+def _time(fn, reps: int, warm_s: float = 0.2, batch_s: float = 2e-3, max_batch: int = 256):
+    """Device seconds per call: each of `reps` samples times a batch of back-to-back calls
+    between two events, so the host's per-call cost (binding + launch, ~15 us) overlaps the
+    previous kernels instead of being counted -- a single call between two events on an
+    idle stream would add it to every small shape's time.  Returns (min, median)."""
     import torch
     t0 = time.time()
-    while time.time() - t0 < warm_s:
+    n = 0
+    while time.time() - t0 < warm_s or n < 2:
         fn()
         torch.cuda.synchronize()
+        n += 1
+    est = (time.time() - t0) / n                   # synced per-call upper bound
+    batch = max(1, min(max_batch, int(batch_s / max(est, 1e-7))))
     ts = []
     for _ in range(reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        fn()
+        for _ in range(batch):
+            fn()
         e1.record()
         torch.cuda.synchronize()
-        ts.append(e0.elapsed_time(e1) * 1e-3)
+        ts.append(e0.elapsed_time(e1) * 1e-3 / batch)
     return min(ts), statistics.median(ts)
 
 
