@@ -14,6 +14,10 @@ Contents
                  star, generalised for alpha/beta:
                    4*K*u*|alpha|*mag + 4*u*|beta|*|C0| + 1e-300,  u = 2^-53
 ``check``        err/bound report: max ratio, worst index, NaN handling.
+``freivalds``    full-coverage exact check of a large result in O(N^2) host work:
+                 (alpha*A*B + beta*C0) x = alpha*A*(B x) + beta*C0 x for random 0/1
+                 matrices x (Eq. (1) applied to vectors; Freivalds' test).  Bitwise
+                 only in the exact (dyadic / small-integer) input regime.
 
 Parity pins for every function here live in ``tests/test_oracle.py``.
 """
@@ -168,3 +172,35 @@ def check(C_test: np.ndarray, C_ref: np.ndarray, bnd: np.ndarray) -> CheckResult
     rel = np.where(nan, np.inf, err / denom)
     return CheckResult(bool(not bad.any()), float(ratio[idx]), tuple(int(v) for v in idx),
                        int(bad.sum()), int(nan.sum()), float(np.median(rel)))
+
+
+def freivalds(alpha: float, beta: float, X: np.ndarray, M: int, K: int, a_rows, b_rows, c_rows, c0_rows=None,
+              chunk: int = 1024) -> np.ndarray:
+    """Rows i of a candidate C (M x n) with C x != alpha*A*(B x) + beta*C0 x, for the n x v
+    0/1 matrix X -- Eq. (1) applied to the columns of X.  Every product is formed
+    on row chunks supplied by callables (the matrices need not fit in memory at once):
+        a_rows(r0, nr)  -> A[r0:r0+nr, :]     (nr x K)
+        b_rows(k0, nk)  -> B[k0:k0+nk, cols]  (nk x n)
+        c_rows(r0, nr)  -> C_test[r0:r0+nr, cols]
+        c0_rows(r0, nr) -> C0[r0:r0+nr, cols] (read only when beta != 0)
+    The comparison is bitwise, so it is valid only where every partial sum is exactly
+    representable: dyadic inputs m/256 (|m| <= 256) with K, n <= 2^16 keep B x below 2^24
+    in units of 2^-8 and A (B x), C x below 2^48 in units of 2^-16 (alpha = 1.5 adds one
+    bit), so any summation order gives the same doubles and a correct C passes exactly.
+    A wrong row i is missed by one random 0/1 column with probability <= 1/2 (Freivalds),
+    by v independent columns with probability <= 2^-v.  Returns the sorted bad row indices."""
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    BX = np.zeros((K, X.shape[1]))
+    for k0 in range(0, K, chunk):
+        nk = min(chunk, K - k0)
+        BX[k0:k0 + nk] = b_rows(k0, nk) @ X
+    bad = []
+    for r0 in range(0, M, chunk):
+        nr = min(chunk, M - r0)
+        rhs = alpha * (a_rows(r0, nr) @ BX)
+        if beta != 0.0:
+            rhs = rhs + beta * (c0_rows(r0, nr) @ X)
+        lhs = c_rows(r0, nr) @ X
+        rows = np.nonzero(np.any(lhs != rhs, axis=1))[0]
+        bad.extend((r0 + rows).tolist())
+    return np.asarray(bad, dtype=np.int64)

@@ -113,18 +113,32 @@ def _check(rc: int):
 
 
 # ------------------------------------------------------------------ tensors
+_DTYPES = {}
+
+
+def _dtype(name):
+    d = _DTYPES.get(name)
+    if d is None:
+        import torch
+        d = _DTYPES[name] = getattr(torch, name)
+    return d
+
+
 def _mat(x, name, dtype="float64"):
-    """(ptr, rows, cols, ld) of a 2-D float64 (or float32) tensor with unit column stride."""
-    if x.dtype.__str__() not in (f"torch.{dtype}", dtype):
+    """(ptr, rows, cols, ld) of a 2-D float64 (or float32) tensor with unit column stride.
+    Per-call cost matters for small GEMMs: one attribute access each (no string work)."""
+    if x.dtype is not _dtype(dtype):
         raise TypeError(f"{name} must be {dtype}, got {x.dtype}")
-    if x.dim() != 2:
+    shp = x.shape
+    if len(shp) != 2:
         raise ValueError(f"{name} must be 2-D")
-    r, c = x.shape
-    if x.numel() == 0:
+    r, c = shp
+    if r == 0 or c == 0:
         return x.data_ptr(), r, c, max(c, 1)
-    if c > 1 and x.stride(1) != 1:
+    s0, s1 = x.stride()
+    if c > 1 and s1 != 1:
         raise ValueError(f"{name} must have unit stride along columns (row-major)")
-    ld = x.stride(0) if (r > 1 or x.stride(0) >= c) else c
+    ld = s0 if (r > 1 or s0 >= c) else c
     ld = max(ld, c, 1)
     return x.data_ptr(), r, c, ld
 

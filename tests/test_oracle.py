@@ -308,3 +308,44 @@ def test_bound_f32_catches_fp32_scale_errors():
     assert oracle.check(np.nextafter(C32.astype(np.float32), np.float32(np.inf)).astype(np.float64), C, bnd).ok
     dropped = oracle.dgemm(1.0, A[:, :-1], B[:-1], 0.0, C0)
     assert not oracle.check(dropped, C, bnd).ok
+
+
+# ---------------------------------------------------------------- Freivalds full-coverage check
+def _freivalds_problem(M, N, K, seed=11, mode="dyadic"):
+    A, B, C0 = synth.problem(M, N, K, mode=mode, seed=seed)
+    X = np.random.default_rng(seed).integers(0, 2, size=(N, 16)).astype(np.float64)
+    return A, B, C0, X
+
+
+def _rows(Mx):
+    return lambda r0, nr: Mx[r0:r0 + nr]
+
+
+def test_freivalds_passes_exact_oracle_result():
+    """Eq. (1) on vectors: the oracle's own exact-regime result satisfies
+    C x == 1.5 A (B x) + 0.5 C0 x bitwise, with chunks that do not divide the sizes."""
+    M, N, K = 150, 97, 130
+    A, B, C0, X = _freivalds_problem(M, N, K)
+    C = oracle.dgemm(1.5, A, B, 0.5, C0)
+    bad = oracle.freivalds(1.5, 0.5, X, M, K, _rows(A), _rows(B), _rows(C), _rows(C0), chunk=37)
+    assert bad.size == 0
+
+
+def test_freivalds_names_a_row_off_by_one_unit():
+    """One entry off by 2^-16 (the granularity of the exact products) is caught and only
+    its row is reported."""
+    M, N, K = 120, 80, 64
+    A, B, C0, X = _freivalds_problem(M, N, K, seed=5)
+    C = oracle.dgemm(1.0, A, B, 0.0, np.zeros((M, N)))
+    C[77, 41] += 2.0 ** -16
+    bad = oracle.freivalds(1.0, 0.0, X, M, K, _rows(A), _rows(B), _rows(C), chunk=50)
+    assert bad.tolist() == [77]
+
+
+def test_freivalds_catches_transposed_operand_and_dropped_beta():
+    M = N = K = 64
+    A, B, C0, X = _freivalds_problem(M, N, K, seed=9)
+    wrong_t = oracle.dgemm(1.0, A, np.ascontiguousarray(B.T), 0.0, np.zeros((M, N)))
+    assert oracle.freivalds(1.0, 0.0, X, M, K, _rows(A), _rows(B), _rows(wrong_t)).size > M // 2
+    no_beta = oracle.dgemm(1.5, A, B, 0.0, np.zeros((M, N)))
+    assert oracle.freivalds(1.5, 0.5, X, M, K, _rows(A), _rows(B), _rows(no_beta), _rows(C0)).size > M // 2
