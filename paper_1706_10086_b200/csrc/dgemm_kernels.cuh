@@ -351,6 +351,10 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
         pol = l2_policy_evict_normal();
+    }
+    griddep_wait();
+    griddep_launch();
+    if (producer) {
         for (int s = 0; s < C::STAGES && s < NK; ++s)
             tma_issue_stage<C>(base_ptr + s * C::STAGE_BYTES, &tmA, &tmB, &full[s], m0, n0, kt0 + s, pol);
     }
@@ -530,6 +534,10 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
         tma_prefetch_desc(&tmB);
         pol = l2_policy_evict_normal();
         pc_coords();
+    }
+    griddep_wait();
+    griddep_launch();
+    if (producer) {
         for (int s = 0; s < C::STAGES && s < nloc; ++s) issue_next(s);
     }
     __syncthreads();
@@ -660,6 +668,10 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
         tma_prefetch_desc(&tmB);
         pol = l2_policy_evict_normal();
         pc_tile(ta);
+    }
+    griddep_wait();
+    griddep_launch();
+    if (producer) {
         for (int s = 0; s < C::STAGES && s < total; ++s) issue_next(s);
     }
     __syncthreads();
@@ -735,6 +747,8 @@ template <class C>
 __global__ void __launch_bounds__(C::CONSUMER_THREADS, 1)
     dgemm_hybrid_fixup_kernel(int M, int N, int K, double alpha, double beta, double *__restrict__ Cm, int64_t ldc,
                               int vec, int group_m, int tdp, int gsk, const double *__restrict__ ws) {
+    griddep_wait();
+    griddep_launch();
     const int tiles_m = (M + C::BM - 1) / C::BM, tiles_n = (N + C::BN - 1) / C::BN;
     const int KT = (K + C::BK - 1) / C::BK;
     const int64_t Ut = (int64_t)(tiles_m * tiles_n - tdp) * KT;
@@ -824,6 +838,8 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, 1)
     const int m0 = tm * C::BM, n0 = tn * C::BN;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int KT = (K + C::BK - 1) / C::BK;
+    griddep_wait();
+    griddep_launch();
 
 #pragma unroll
     for (int s = 0; s < C::STAGES - 1; ++s) {

@@ -54,6 +54,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 }
 
+// ---- programmatic dependent launch (PDL) -------------------------------------------
+// The host launches every GEMM kernel with programmatic stream serialization, so a kernel
+// may become resident while the previous kernel in the stream is still draining.  Each
+// kernel sets up its shared-memory state, then griddep_wait() blocks until the previous
+// grid has completed and its memory is visible -- before the first global access -- and
+// griddep_launch() lets the next kernel start its own setup early (it still waits in turn).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 // ---- TMA ------------------------------------------------------------------------
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap *map) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");

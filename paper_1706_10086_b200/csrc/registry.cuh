@@ -1,7 +1,9 @@
 // registry.cuh -- configuration table entries and the launch templates.
 #pragma once
 #include <algorithm>
+#include <cstdlib>
 #include <cuda.h>
+#include <utility>
 #include <cuda_runtime.h>
 
 #include "../../include/gemm_f64.h"
@@ -33,6 +35,34 @@ struct CfgEntry {
     int (*launch)(const LaunchArgs &, cudaStream_t);
 };
 
+// Every GEMM kernel is launched with programmatic stream serialization (PDL): it may become
+// resident while the previous kernel of the stream drains and waits for it in-kernel
+// (griddep_wait in ptx.cuh) before touching global memory.  GEMM_PDL=0 in the environment
+// launches them the classic way (A/B measurements).
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char *e = std::getenv("GEMM_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 template <class C, bool SPLIT, bool XP>
 static int launch_tma(const LaunchArgs &a, cudaStream_t st) {
     CUtensorMap ta, tb;
@@ -43,18 +73,19 @@ static int launch_tma(const LaunchArgs &a, cudaStream_t st) {
     const int64_t tiles = ((int64_t)a.M + C::BM - 1) / C::BM * (((int64_t)a.N + C::BN - 1) / C::BN);
     if (tiles > 0x7FFFFFFF) return set_error(GEMM_ERR_UNSUPPORTED, "too many tiles (%lld)", (long long)tiles);
     dim3 grid((unsigned)tiles, SPLIT ? a.sk.splits : 1);
-    dgemm_tma_kernel<C, SPLIT, XP><<<grid, C::CONSUMER_THREADS, C::SMEM_BYTES, st>>>(
-        ta, tb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec, a.group_m, a.sk);
-    return cuda_check(cudaGetLastError(), "dgemm_tma_kernel launch");
+    return cuda_check(launch_k(dgemm_tma_kernel<C, SPLIT, XP>, grid, dim3(C::CONSUMER_THREADS), C::SMEM_BYTES, st,
+                               ta, tb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec, a.group_m, a.sk),
+                      "dgemm_tma_kernel launch");
 }
 
 template <class C>
 static int launch_generic(const LaunchArgs &a, cudaStream_t st) {
     const int64_t tiles = ((int64_t)a.M + C::BM - 1) / C::BM * (((int64_t)a.N + C::BN - 1) / C::BN);
     if (tiles > 0x7FFFFFFF) return set_error(GEMM_ERR_UNSUPPORTED, "too many tiles (%lld)", (long long)tiles);
-    dgemm_generic_kernel<C><<<(unsigned)tiles, C::CONSUMER_THREADS, C::SMEM_BYTES, st>>>(
-        a.A, a.lda, a.B, a.ldb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec, a.group_m);
-    return cuda_check(cudaGetLastError(), "dgemm_generic_kernel launch");
+    return cuda_check(launch_k(dgemm_generic_kernel<C>, dim3((unsigned)tiles), dim3(C::CONSUMER_THREADS),
+                               C::SMEM_BYTES, st, a.A, a.lda, a.B, a.ldb, a.M, a.N, a.K, a.alpha, a.beta, a.C,
+                               a.ldc, a.vec, a.group_m),
+                      "dgemm_generic_kernel launch");
 }
 
 // Stream-K launch: grid = min(U, SMs x resident CTAs); workspace = 2 partial slots per CTA.
@@ -79,9 +110,9 @@ static int launch_streamk(const LaunchArgs &a, cudaStream_t st) {
     int *ctr = nullptr;
     rc = streamk_workspace(st, (size_t)C::BM * C::BN, grid, (size_t)tiles, &ws, &ctr);
     if (rc) return rc;
-    dgemm_streamk_kernel<C><<<grid, C::CONSUMER_THREADS, C::SMEM_BYTES, st>>>(
-        ta, tb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec, a.group_m, ws, ctr);
-    return cuda_check(cudaGetLastError(), "dgemm_streamk_kernel launch");
+    return cuda_check(launch_k(dgemm_streamk_kernel<C>, dim3(grid), dim3(C::CONSUMER_THREADS), C::SMEM_BYTES, st,
+                               ta, tb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec, a.group_m, ws, ctr),
+                      "dgemm_streamk_kernel launch");
 }
 
 // Hybrid launch: the W full data-parallel waves as one plain XP launch (grid = W*G tiles),
@@ -106,9 +137,10 @@ static int launch_hybrid(const LaunchArgs &a, cudaStream_t st) {
     const int64_t tdp = tiles / G * G, tail = tiles - tdp;
     if (tdp > 0) {
         SplitArgs none{1, nullptr, nullptr};
-        dgemm_tma_kernel<C, false, true><<<(unsigned)tdp, C::CONSUMER_THREADS, C::SMEM_BYTES, st>>>(
-            ta, tb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec, a.group_m, none);
-        rc = cuda_check(cudaGetLastError(), "hybrid data-parallel launch");
+        rc = cuda_check(launch_k(dgemm_tma_kernel<C, false, true>, dim3((unsigned)tdp), dim3(C::CONSUMER_THREADS),
+                                 C::SMEM_BYTES, st, ta, tb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec,
+                                 a.group_m, none),
+                        "hybrid data-parallel launch");
         if (rc || tail == 0) return rc;
     }
     HybArgs hy{(int)tdp, 0, nullptr};
@@ -117,14 +149,15 @@ static int launch_hybrid(const LaunchArgs &a, cudaStream_t st) {
     int *ctr = nullptr;
     rc = streamk_workspace(st, (size_t)C::BM * C::BN, hy.gsk, 0, &hy.ws, &ctr);
     if (rc) return rc;
-    dgemm_sktail_kernel<C><<<hy.gsk, C::CONSUMER_THREADS, C::SMEM_BYTES, st>>>(
-        ta, tb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec, a.group_m, hy);
-    rc = cuda_check(cudaGetLastError(), "dgemm_sktail_kernel launch");
+    rc = cuda_check(launch_k(dgemm_sktail_kernel<C>, dim3(hy.gsk), dim3(C::CONSUMER_THREADS), C::SMEM_BYTES, st, ta,
+                             tb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec, a.group_m, hy),
+                    "dgemm_sktail_kernel launch");
     if (rc || ((int64_t)hy.gsk == tail && Ut % hy.gsk == 0)) return rc;   // every tail CTA had a whole tile
     static_assert((C::MB * C::NP) % kFixQ == 0, "fix-up quad split");
-    dgemm_hybrid_fixup_kernel<C><<<dim3((unsigned)tail, C::MB * C::NP / kFixQ), C::CONSUMER_THREADS, 0, st>>>(
-        a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec, a.group_m, (int)tdp, hy.gsk, hy.ws);
-    return cuda_check(cudaGetLastError(), "dgemm_hybrid_fixup_kernel launch");
+    return cuda_check(launch_k(dgemm_hybrid_fixup_kernel<C>, dim3((unsigned)tail, C::MB * C::NP / kFixQ),
+                               dim3(C::CONSUMER_THREADS), 0, st, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec,
+                               a.group_m, (int)tdp, hy.gsk, (const double *)hy.ws),
+                      "dgemm_hybrid_fixup_kernel launch");
 }
 
 #define DG_HYB(BM, BN, BK, WM, WN, ST)                                                                       \
