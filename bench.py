@@ -33,6 +33,9 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# NCCL writes its version banner to stdout at communicator init unless told otherwise;
+# rank 0's stdout carries exactly one JSON line (an explicit NCCL_DEBUG is left alone)
+os.environ.setdefault("NCCL_DEBUG", "WARN")
 
 METRIC = "DGEMM TFLOP/s and % of B200 FP64 peak at N=16384 (1 GPU) and 1/2/4/8 GPUs"
 FP64_DATASHEET_TFLOPS = 37.0      # HGX B200: 296 TFLOP/s FP64 / FP64 tensor per 8 GPUs
