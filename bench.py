@@ -33,9 +33,6 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-# NCCL writes its version banner to stdout at communicator init unless told otherwise;
-# rank 0's stdout carries exactly one JSON line (an explicit NCCL_DEBUG is left alone)
-os.environ.setdefault("NCCL_DEBUG", "WARN")
 
 METRIC = "DGEMM TFLOP/s and % of B200 FP64 peak at N=16384 (1 GPU) and 1/2/4/8 GPUs"
 FP64_DATASHEET_TFLOPS = 37.0      # HGX B200: 296 TFLOP/s FP64 / FP64 tensor per 8 GPUs
@@ -58,6 +55,21 @@ def parse():
     if a.warmup < 3:
         a.warmup = 3
     return a
+
+
+def stdout_to_stderr(fn):
+    """Run fn with the process's C-level stdout (fd 1) pointed at stderr: NCCL prints its
+    version banner on stdout when a communicator is created, and rank 0's stdout must carry
+    exactly one line, the JSON result."""
+    sys.stdout.flush()
+    saved = os.dup(1)
+    try:
+        os.dup2(2, 1)
+        return fn()
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved, 1)
+        os.close(saved)
 
 
 def workload(name, world):
@@ -255,7 +267,7 @@ def main():
     # the same code as N>1 (an in-place 1-rank broadcast is a no-op)
     distributed = world > 1 or "TORCHELASTIC_RUN_ID" in os.environ or "GEMM_BENCH_FORCE_DIST" in os.environ
     if distributed:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        stdout_to_stderr(lambda: dist.init_process_group("nccl", device_id=torch.device("cuda", local)))
 
     M, N, K, scaling, wname = workload(a.workload, world)
     r0, r1 = G.row_range(M, rank, world)
@@ -270,7 +282,27 @@ def main():
         dB.zero_()
     G.fill(dC, "uniform", 1706, 2, rows=M, row0=r0)
     stream = torch.cuda.current_stream()
-    comm = G.Comm(rank, world) if distributed else None
+    # B's broadcast goes through the library's own NCCL communicator (gemm_comm_init).  If that
+    # cannot be created on some rank, every rank falls back to the same NCCL broadcast through
+    # torch's process group, so the scaling run still measures the sharded path; the line says so.
+    comm, bcast_via = None, None
+    if distributed:
+        err = None
+        try:
+            if os.environ.get("GEMM_BENCH_TORCH_BCAST"):   # exercise the fallback (tests)
+                raise RuntimeError("forced by GEMM_BENCH_TORCH_BCAST")
+            comm = stdout_to_stderr(lambda: G.Comm(rank, world))
+        except Exception as ex:  # noqa: BLE001 -- reported in the JSON line
+            err = f"{type(ex).__name__}: {ex}"[:200]
+        ok = torch.tensor([0.0 if err else 1.0], device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if ok.item() < 1.0:
+            if comm is not None:
+                comm.close()
+            comm = None
+            bcast_via = "torch.distributed NCCL broadcast (library communicator failed: " + (err or "on another rank") + ")"
+        else:
+            bcast_via = "libgemm_f64 NCCL communicator (gemm_bcast_f64)"
     # the product's own plan (heuristic entry point) unless a configuration is forced
     cfg = a.cfg if a.cfg >= 0 else None
     plan_cfg, plan_splits = G.plan(Ml, N, K, dA.data_ptr(), K, dB.data_ptr(), N)
@@ -283,6 +315,8 @@ def main():
     def step(evs=None):
         if comm is not None:
             comm.bcast(dB, root=0, stream=stream)
+        elif distributed:
+            dist.broadcast(dB, src=0)
         if evs is not None:
             evs[0].record(stream)
         G.gemm(dA, dB, dC, 1.0, 0.0, cfg=cfg, stream=stream)
@@ -378,7 +412,8 @@ def main():
                 "config": {"workload": wname, "M": M, "N": N, "K": K, "rows_per_gpu": Ml, "alpha": 1.0,
                            "beta": 0.0, "inputs": "seeded uniform[-1,1) (synth generator, device fill)",
                            "l2": "inputs larger than L2 (no flush)", "kernel_cfg": cfg_name,
-                           "parallelism": f"row-sharded x{world}, B broadcast (NCCL)" if world > 1 else "1 GPU"},
+                           "parallelism": f"row-sharded x{world}, B broadcast (NCCL)" if world > 1 else "1 GPU",
+                           "bcast": bcast_via},
                 "pct_of_fp64_peak": 100.0 * value / (FP64_DATASHEET_TFLOPS * world),
                 "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": a.steps * launches_per_step}
