@@ -110,3 +110,18 @@ def test_freivalds_config5_rank_shard_column_block(cuda_lib):
     """Config 5 (N=65536) as one rank of the 8-GPU run computes it: global rows
     [57344, 65536) (rank 7), all 8192 rows x a 2048-column block (16.8M entries), K=65536."""
     _check(cuda_lib, 8192, 65536, 65536, 1.0, 0.0, seed=24, c0=30720, nc=2048, rows_total=65536, row0=57344)
+
+
+@pytest.mark.parametrize("shape", [(1024, 1024, 1024), (2048, 2048, 2048), (4096, 4096, 4096), (3000, 5000, 2000),
+                                   (1536, 1536, 1536), (700, 9000, 3000)], ids=lambda s: "x".join(map(str, s)))
+def test_freivalds_config2_and_ragged_every_entry(cuda_lib, shape):
+    """Config-2 sizes and ragged shapes with whatever plan the product picks (split-K,
+    hybrid, XP): every entry, alpha=1.5, beta=0.5."""
+    M, N, K = shape
+    _check(cuda_lib, M, N, K, 1.5, 0.5, seed=M + N + K)
+
+
+def test_freivalds_odd_leading_dimension_repack_every_entry(cuda_lib):
+    """Odd K and N: no TMA on the caller's buffers, so the product repacks them into aligned
+    workspace and runs the TMA path (10000 x 9999 x 7001, the repack test shape)."""
+    _check(cuda_lib, 10000, 9999, 7001, 1.5, 0.5, seed=31)
