@@ -343,9 +343,15 @@ static Choice choose_uncached(int64_t M, int64_t N, int64_t K, bool tma, bool si
             continue;
         }
         if (d.split_k == -1) {   // stream-K: every CTA gets ceil(U/G) k-steps, no partial waves
+            // + the same per-tile cost as the data-parallel model (4 k-steps: pipeline fill and
+            // epilogue) for each tile a CTA touches: with short K a CTA's range covers many
+            // tiles, and without this term stream-K won shapes it loses by 3-6 %
+            // (profiles/r01_heuristic_regret.csv)
             const int64_t tiles = ((M + d.bm - 1) / d.bm) * ((N + d.bn - 1) / d.bn);
             const int64_t G = std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * occ, tiles * KT));
-            const double t = ((double)((tiles * KT + G - 1) / G) + 6.0) * occ * d.bm * d.bn * (d.bk / 16.0) / c.eff;
+            const double per_cta_tiles = (double)((tiles + G - 1) / G) + 1.0;
+            const double t = ((double)((tiles * KT + G - 1) / G) + 4.0 * per_cta_tiles + 6.0) * occ * d.bm * d.bn *
+                             (d.bk / 16.0) / c.eff;
             if (t < best_t * 0.999) {
                 best_t = t;
                 best.id = id;
