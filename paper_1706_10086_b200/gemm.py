@@ -143,10 +143,26 @@ def _mat(x, name, dtype="float64"):
     return x.data_ptr(), r, c, ld
 
 
+_RAW_STREAM = None
+
+
+def _current_raw_stream():
+    """cudaStream_t of torch's current stream on the current device.  torch's raw-pointer
+    query (what Triton's launcher uses) costs ~0.3 us against ~3 us for building a
+    torch.cuda.Stream object, a large share of a small GEMM's host cost; the public API is
+    the fallback if the private one is absent."""
+    global _RAW_STREAM
+    import torch
+    if _RAW_STREAM is None:
+        raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+        _RAW_STREAM = (lambda: raw(torch.cuda.current_device())) if raw is not None else \
+            (lambda: torch.cuda.current_stream().cuda_stream)
+    return _RAW_STREAM()
+
+
 def _stream_ptr(stream):
     if stream is None:
-        import torch
-        return torch.cuda.current_stream().cuda_stream
+        return _current_raw_stream()
     if isinstance(stream, int):
         return stream
     return stream.cuda_stream
