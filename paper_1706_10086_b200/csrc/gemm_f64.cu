@@ -234,7 +234,7 @@ static bool tma_ok(const double *A, int64_t lda, const double *B, int64_t ldb) {
 // (a CTA's k-steps plus ~4 k-steps of pipeline fill and epilogue, +2 for a split-K
 // reduction), eff = the configuration's measured steady-state efficiency
 // (profiles/r01_scale_allcfgs.csv, r01_tune_n8192_a1.5_b0.5.csv).  Split-K candidates
-// try S = 1..16 with at least 4 k-steps per split.
+// try S = 1..16 with at least 2 k-steps per split.
 struct Cand {
     const char *name;
     double eff;
@@ -359,7 +359,7 @@ static Choice choose_uncached(int64_t M, int64_t N, int64_t K, bool tma, bool si
             }
             continue;
         }
-        const int smax = d.split_k == 1 ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(16, KT / 4));
+        const int smax = d.split_k == 1 ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(16, KT / 2));
         for (int S = 1; S <= smax; ++S) {
             const double t = est_time(d, occ, sms, M, N, K, S, c.eff);
             if (t < best_t * 0.999) {
@@ -385,7 +385,7 @@ static int auto_splits(int id, int64_t M, int64_t N, int64_t K) {
     const gemm_cfg_desc &d = g_cfgs[id].d;
     if (d.split_k > 1) return d.split_k;
     const int64_t KT = (K + d.bk - 1) / d.bk;
-    const int smax = (int)std::max<int64_t>(1, std::min<int64_t>(16, KT / 4));
+    const int smax = (int)std::max<int64_t>(1, std::min<int64_t>(16, KT / 2));
     int bestS = 1;
     double bt = 1e300;
     for (int S = 1; S <= smax; ++S) {

@@ -39,7 +39,7 @@ def candidates(M: int, N: int, K: int, tma: bool = True):
         else:
             kt = (K + info["bk"] - 1) // info["bk"]
             for s in (1, 2, 3, 4, 6, 8, 12, 16):
-                if s == 1 or (s <= kt // 4 and tiles_small * s <= 8 * 148 * 2):
+                if s == 1 or (s <= kt // 2 and tiles_small * s <= 8 * 148 * 2):
                     out.append((info["id"], s))
     return out
 
