@@ -23,6 +23,7 @@ static const CfgEntry k_table[] = {
     DG_TMA_SPLIT(128, 128, 16, 32, 32, 4),
     DG_SK(64, 64, 16, 32, 16, 6),
     DG_SK(128, 64, 16, 32, 16, 6),
+    DG_HYB(64, 64, 16, 32, 16, 6),
 };
 
 const CfgEntry *cfg_table_small(int *n) {

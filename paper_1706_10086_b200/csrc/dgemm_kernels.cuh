@@ -96,6 +96,19 @@ struct FragOffsets {
     }
 };
 
+// A warp hands a ring slot back to the producer.  Its fragment loads of the slot are
+// generic-proxy reads and the refill is an async-proxy (TMA) write, so every lane fences
+// (fence.proxy.async: its prior shared-memory accesses are performed and ordered before
+// async-proxy accesses) before lane 0 arrives on the slot's `empty` barrier.  Without the
+// fence the arrive can overtake the warp's last LDS of the slot (ptxas places it before the
+// stage's last DMMAs); measured: once the refill was issued by a warp other than the laggard,
+// split-K results picked up k-steps from the next lap of the ring.
+__device__ __forceinline__ void release_slot(uint64_t *empty_bar, int lane) {
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty_bar);
+}
+
 // One pipeline stage of the warp's register-blocked tile multiply (row a3).
 template <class C>
 __device__ __forceinline__ void mma_stage(uint32_t sA, uint32_t sB, const FragOffsets<C> &fo,
@@ -316,7 +329,10 @@ __device__ __forceinline__ bool split_reduce(double (&acc)[C::MB][C::NP][2][2], 
 // XP = true: cross-stage fragment prefetch -- the first half of stage i+1 is loaded (after
 // its full-barrier wait) before the last half of stage i is multiplied, so the DMMA pipe
 // does not drain at stage boundaries.
-template <class C, bool SPLIT, bool XP>
+// ROT > 1: the refill of k-step i is issued by lane 0 of warp i % ROT instead of always by
+// warp 0, spreading the producer's per-k-step instructions over ROT warps (and so over the
+// SM's sub-partitions); the ring protocol is unchanged.
+template <class C, bool SPLIT, bool XP, int ROT = 1>
 __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
     dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
                      int N, int K, double alpha, double beta, double *__restrict__ Cm, int64_t ldc, int vec,
@@ -339,6 +355,7 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
     const int kt0 = (int)(((int64_t)split * KT) / nsplit);
     const int NK = (int)(((int64_t)(split + 1) * KT) / nsplit) - kt0;   // k-steps of this CTA
     const bool producer = (threadIdx.x == 0);
+    constexpr int R = ROT < C::CONSUMER_WARPS ? ROT : C::CONSUMER_WARPS;   // warps sharing the refills
     uint64_t pol = 0;
 
     if (producer) {
@@ -350,8 +367,8 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
         fence_mbar_init();
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
-        pol = l2_policy_evict_normal();
     }
+    if (R > 1 ? lane == 0 : producer) pol = l2_policy_evict_normal();
     griddep_wait();
     griddep_launch();
     if (producer) {
@@ -373,7 +390,8 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
     if constexpr (!XP) {
         for (int i = 0; i < NK; ++i) {
             const int s = i % C::STAGES;
-            if (producer && i > 0) {
+            const bool refill = R > 1 ? (lane == 0 && warp == i % R) : producer;
+            if (refill && i > 0) {
                 const int in = i - 1 + C::STAGES;   // refill the slot released at i-1
                 if (in < NK) {
                     const int sp = (i - 1) % C::STAGES;
@@ -382,11 +400,11 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
                                        pol);
                 }
             }
+            if (R > 1) __syncwarp();   // the refilling lane rejoins before the warp-wide mma.sync
             mbar_wait(&full[s], (i / C::STAGES) & 1);
             const uint32_t sA = base + s * C::STAGE_BYTES;
             mma_stage<C>(sA, sA + C::A_BYTES, fo, acc);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
+            release_slot(&empty[s], lane);
         }
     } else {
         constexpr int H = 2 * C::KG;   // halves per stage (even: half 0 of every stage uses f[0])
@@ -397,7 +415,8 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
         }
         for (int i = 0; i < NK; ++i) {
             const int s = i % C::STAGES;
-            if (producer && i > 0) {
+            const bool refill = R > 1 ? (lane == 0 && warp == i % R) : producer;
+            if (refill && i > 0) {
                 const int in = i - 1 + C::STAGES;
                 if (in < NK) {
                     const int sp = (i - 1) % C::STAGES;
@@ -406,21 +425,26 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
                                        pol);
                 }
             }
+            if (R > 1) __syncwarp();   // the refilling lane rejoins before the warp-wide mma.sync
             const uint32_t sA = base + s * C::STAGE_BYTES;
 #pragma unroll
             for (int h = 0; h < H; ++h) {
                 if (h + 1 < H) {
                     load_half<C>(sA, sA + C::A_BYTES, h + 1, fo, f[(h + 1) & 1]);
-                } else if (i + 1 < NK) {
-                    const int s1 = (i + 1) % C::STAGES;
-                    mbar_wait(&full[s1], ((i + 1) / C::STAGES) & 1);
-                    const uint32_t sA1 = base + s1 * C::STAGE_BYTES;
-                    load_half<C>(sA1, sA1 + C::A_BYTES, 0, fo, f[0]);
+                } else {
+                    // every fragment of slot s has been requested: hand the slot back before
+                    // the next stage's loads are issued, so the release fence waits only
+                    // for this slot's last half (needed by the DMMAs below anyway)
+                    release_slot(&empty[s], lane);
+                    if (i + 1 < NK) {
+                        const int s1 = (i + 1) % C::STAGES;
+                        mbar_wait(&full[s1], ((i + 1) / C::STAGES) & 1);
+                        const uint32_t sA1 = base + s1 * C::STAGE_BYTES;
+                        load_half<C>(sA1, sA1 + C::A_BYTES, 0, fo, f[0]);
+                    }
                 }
                 mma_half<C>(f[h & 1], acc);
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
         }
     }
     if constexpr (SPLIT) {
@@ -568,8 +592,7 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
             mbar_wait(&full[stage], (uint32_t)phase);
             const uint32_t sA = base + stage * C::STAGE_BYTES;
             mma_stage<C>(sA, sA + C::A_BYTES, fo, acc);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[stage]);
+            release_slot(&empty[stage], lane);
             if (++stage == C::STAGES) {
                 stage = 0;
                 phase ^= 1;
@@ -710,15 +733,16 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
             for (int h = 0; h < H; ++h) {
                 if (h + 1 < H) {
                     load_half<C>(sA, sA + C::A_BYTES, h + 1, fo, f[(h + 1) & 1]);
-                } else if (i + 1 < NK) {   // cross-stage prefetch inside the segment
-                    mbar_wait(&full[s1], (uint32_t)p1);
-                    const uint32_t sA1 = base + s1 * C::STAGE_BYTES;
-                    load_half<C>(sA1, sA1 + C::A_BYTES, 0, fo, f[0]);
+                } else {
+                    release_slot(&empty[stage], lane);   // as in dgemm_tma_kernel (XP)
+                    if (i + 1 < NK) {   // cross-stage prefetch inside the segment
+                        mbar_wait(&full[s1], (uint32_t)p1);
+                        const uint32_t sA1 = base + s1 * C::STAGE_BYTES;
+                        load_half<C>(sA1, sA1 + C::A_BYTES, 0, fo, f[0]);
+                    }
                 }
                 mma_half<C>(f[h & 1], acc);
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[stage]);
             stage = s1;
             phase = p1;
         }

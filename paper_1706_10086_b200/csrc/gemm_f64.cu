@@ -9,6 +9,8 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -240,13 +242,15 @@ struct Cand {
     double eff;
 };
 static const Cand k_tma_cands[] = {
-    {"tma_256x64x16_w64x32_s4_xp", 0.981},     {"tma_128x128x16_w64x32_s4_xp", 0.979},
+    // eff = measured fraction of the clock roof at 16384^3 (profiles/r01_f2_tuner_table_run_v7.log)
+    {"tma_256x64x16_w64x32_s4_xp", 0.979},     {"tma_128x128x16_w64x32_s4_xp", 0.980},
     {"tma_256x64x16_w64x32_s4_hybrid", 0.981},
-    {"tma_64x128x16_w32x64_s4", 0.972},
-    {"tma_128x128x16_w32x32_s4", 0.965},       {"tma_64x64x16_w32x16_s6", 0.952},
-    {"tma_64x64x16_w32x16_s6_splitk", 0.950},  {"tma_128x64x16_w32x16_s6_splitk", 0.945},
-    {"tma_64x128x16_w32x64_s4_splitk", 0.965}, {"tma_128x128x16_w32x32_s4_splitk", 0.960},
-    {"tma_128x64x16_w32x16_s6_streamk", 0.935}, {"tma_64x64x16_w32x16_s6_streamk", 0.920},
+    {"tma_64x128x16_w32x64_s4", 0.986},
+    {"tma_128x128x16_w32x32_s4", 0.973},       {"tma_64x64x16_w32x16_s6", 0.988},
+    {"tma_64x64x16_w16x32_s6", 0.991},
+    {"tma_64x64x16_w32x16_s6_splitk", 0.992},  {"tma_128x64x16_w32x16_s6_splitk", 0.982},
+    {"tma_64x128x16_w32x64_s4_splitk", 0.981}, {"tma_128x128x16_w32x32_s4_splitk", 0.971},
+    {"tma_128x64x16_w32x16_s6_streamk", 0.920}, {"tma_64x64x16_w32x16_s6_streamk", 0.852},
 };
 
 struct Choice {
@@ -515,6 +519,24 @@ int validate(int64_t M, int64_t N, int64_t K, double alpha, const double *A, int
     return GEMM_OK;
 }
 
+// Grouped raster (a1): consecutive CTAs walk group_m tile-rows column by column, so the
+// CTAs resident at one time cover about group_m x (G / group_m) tiles (G = SMs x CTAs per
+// SM) and share their A row panels and B column panels in L2 at each k-step.  The region's
+// k-slice bytes, 8*BK*(group_m*BM + (G/group_m)*BN), are smallest for a region that is
+// square in elements: group_m = sqrt(G*BN/BM) (8 for 256x64 tiles at 1 CTA/SM, 17 for
+// 64x64 at 2).  GEMM_GROUP_M overrides it (measurements).
+static int raster_group(const gemm_cfg_desc &d, int occ, int64_t M) {
+    static const int forced = [] {
+        const char *e = std::getenv("GEMM_GROUP_M");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (forced > 0) return forced;
+    const double G = (double)num_sms() * (occ > 0 ? occ : 1);
+    int g = (int)std::lround(std::sqrt(G * d.bn / d.bm));
+    const int64_t tiles_m = (M + d.bm - 1) / d.bm;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(g, std::max<int64_t>(1, tiles_m)));
+}
+
 int gemm_impl(int64_t M, int64_t N, int64_t K, double alpha, const double *A, int64_t lda, const double *B,
               int64_t ldb, double beta, double *C, int64_t ldc, int cfg_id, cudaStream_t st, int force_splits) {
     clear_error();
@@ -581,7 +603,8 @@ int gemm_impl(int64_t M, int64_t N, int64_t K, double alpha, const double *A, in
                          g_cfgs[id].name, (int)((uintptr_t)A % 16), (int)((uintptr_t)B % 16), (long long)lda,
                          (long long)ldb);
     }
-    rc = prepare_cfg(id);
+    int occ = 1;
+    rc = prepare_cfg(id, &occ);
     if (rc) return rc;
     const gemm_cfg_desc &d = g_cfgs[id].d;
     if (force_splits < 0) return set_error(GEMM_ERR_ARG, "splits=%d must be >= 0", force_splits);
@@ -598,7 +621,7 @@ int gemm_impl(int64_t M, int64_t N, int64_t K, double alpha, const double *A, in
         sk.splits = splits;
     }
     LaunchArgs a{(int)M, (int)N, (int)K, alpha, beta, A, lda, B, ldb, C, ldc,
-                 ((uintptr_t)C % 32 == 0 && ldc % 4 == 0) ? 1 : 0, 8, sk};
+                 ((uintptr_t)C % 32 == 0 && ldc % 4 == 0) ? 1 : 0, raster_group(d, occ, M), sk};
     return g_cfgs[id].launch(a, st);
 }
 

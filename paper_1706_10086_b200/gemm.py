@@ -299,12 +299,15 @@ def launches_per_call(cfg: int, M: int, N: int, K: int, sms: int = 148) -> int:
     """Kernels one gemm call with configuration `cfg` launches (alpha != 0, K > 0): 1 for the
     one-kernel schedules (plain, split-K with in-kernel reduction, stream-K); the hybrid
     (split_k = -2) launches the data-parallel waves, the stream-K tail and the tail fix-up,
-    each only when needed (mirrors launch_hybrid in csrc/registry.cuh; one CTA per SM)."""
+    each only when needed (mirrors launch_hybrid in csrc/registry.cuh; the waves hold
+    SMs x CTAs-per-SM tiles)."""
     d = cfg_info(cfg)
     if d["split_k"] != -2:
         return 1
     tiles = -(-M // d["bm"]) * -(-N // d["bn"])
     kt = -(-K // d["bk"])
+    occ = 2 if 2 * (d["smem_bytes"] + 1024) <= 228 * 1024 else 1   # Cfg::MIN_BLOCKS (dgemm_kernels.cuh)
+    sms = sms * occ
     tdp = tiles // sms * sms
     tail = tiles - tdp
     if tail == 0:

@@ -116,7 +116,12 @@ def test_cfg_registry(G):
 
 def test_heuristic_selection(G):
     big = G.cfg_info(G.cfg_select(16384, 16384, 16384, 0, 16384, 0, 16384))
-    assert big["tma"] == 1 and big["bm"] * big["bn"] >= 128 * 128
+    assert big["tma"] == 1 and big["e"] >= 16
+    # the tuned table (loaded by the binding) pins the measured best plan for the bench shape
+    table = [ln.split() for ln in open(os.path.join(os.path.dirname(G.__file__), "tuned_b200.txt"))
+             if ln.strip() and not ln.startswith("#")]
+    pinned = [t[4] for t in table if t[:3] == ["16384", "16384", "16384"]]
+    assert pinned and big["name"] == pinned[0]
     odd = G.cfg_info(G.cfg_select(1000, 1000, 1001, 0, 1001, 0, 1000))
     assert odd["tma"] == 0       # odd lda -> not TMA-eligible
     mis = G.cfg_info(G.cfg_select(4096, 4096, 4096, 8, 4096, 0, 4096))

@@ -611,19 +611,18 @@ def _tile_coords(bid, tiles_m, tiles_n, group_m=8):
 
 @pytest.mark.parametrize("shape", [(16384, 4096, 4096), (7168, 7168, 7168)], ids=lambda s: "x".join(map(str, s)))
 def test_hybrid_plan_full_size_tail_rows(cuda_lib, shape):
-    """Full-size shapes the product runs with the hybrid schedule (config-4 2-GPU shard,
-    the f1 grid): rows through the stream-K tail tiles (cut between CTAs, finished by the
-    fix-up kernel) and through data-parallel tiles, checked against the oracle."""
+    """Full-size shapes through the hybrid schedule (config-4 2-GPU shard, the f1 grid; the
+    product's plan for some shapes): rows through the stream-K tail tiles (cut between CTAs,
+    finished by the fix-up kernel) and through data-parallel tiles, checked against the oracle."""
     M, N, K = shape
     dA = torch.empty((M, K), dtype=torch.float64, device="cuda")
     dB = torch.empty((K, N), dtype=torch.float64, device="cuda")
     dC = torch.empty((M, N), dtype=torch.float64, device="cuda")
-    cid, _ = cuda_lib.plan(M, N, K, dA.data_ptr(), K, dB.data_ptr(), N)
-    assert cuda_lib.cfg_name(cid).endswith("_hybrid"), cuda_lib.cfg_name(cid)
+    hyb = cuda_lib.cfg_id("tma_256x64x16_w64x32_s4_hybrid")
     cuda_lib.fill(dA, "uniform", 1706, 0)
     cuda_lib.fill(dB, "uniform", 1706, 1)
     cuda_lib.fill(dC, "uniform", 1706, 2)
-    cuda_lib.gemm(dA, dB, dC, 1.5, 0.5)
+    cuda_lib.gemm(dA, dB, dC, 1.5, 0.5, cfg=hyb)
     torch.cuda.synchronize()
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     tm_n, tn_n = (M + 255) // 256, (N + 63) // 64
