@@ -240,14 +240,15 @@ static bool tma_ok(const double *A, int64_t lda, const double *B, int64_t ldb) {
 struct Cand {
     const char *name;
     double eff;
+    double eff_tail = 0.0;   // hybrid: efficiency of its stream-K tail kernel (0: same as eff)
 };
 static const Cand k_tma_cands[] = {
     // eff = measured fraction of the clock roof at 16384^3 (profiles/r01_f2_tuner_table_run_v7.log)
     {"tma_256x64x16_w64x32_s4_xp", 0.979},     {"tma_128x128x16_w64x32_s4_xp", 0.980},
-    {"tma_256x64x16_w64x32_s4_hybrid", 0.981},
+    {"tma_256x64x16_w64x32_s4_hybrid", 0.981, 0.966},
     {"tma_64x128x16_w32x64_s4", 0.986},
     {"tma_128x128x16_w32x32_s4", 0.973},       {"tma_64x64x16_w32x16_s6", 0.988},
-    {"tma_64x64x16_w16x32_s6", 0.991},        {"tma_64x64x16_w32x16_s6_hybrid", 0.990},
+    {"tma_64x64x16_w16x32_s6", 0.991},        {"tma_64x64x16_w32x16_s6_hybrid", 0.990, 0.85},
     {"tma_64x64x16_w32x16_s6_splitk", 0.992},  {"tma_128x64x16_w32x16_s6_splitk", 0.982},
     {"tma_64x128x16_w32x64_s4_splitk", 0.981}, {"tma_128x128x16_w32x32_s4_splitk", 0.971},
     {"tma_128x64x16_w32x16_s6_streamk", 0.920}, {"tma_64x64x16_w32x16_s6_streamk", 0.852},
@@ -333,12 +334,15 @@ static Choice choose_uncached(int64_t M, int64_t N, int64_t K, bool tma, bool si
             const int64_t tiles = ((M + d.bm - 1) / d.bm) * ((N + d.bn - 1) / d.bn);
             const int64_t G = (int64_t)sms * occ;
             const int64_t W = tiles / G, tail = tiles - W * G;
-            double ks = (double)W * (double)(KT + 4);
+            // the full waves run at the data-parallel kernel's efficiency, the tail at its
+            // stream-K kernel's (lower for the E=16 warp tiles: without it the model sent
+            // skinny and K-heavy shapes to the 64x64 hybrid, 6-12 % slower than the best)
+            double ks = (double)W * (double)(KT + 4) / c.eff;
             if (tail > 0) {   // + pipeline fill, partial store, fix-up and two launch gaps
                 const int64_t gsk = std::min<int64_t>(G, std::max<int64_t>(tail, tail * KT / 16));
-                ks += (double)((tail * KT + gsk - 1) / gsk) + 12.0;
+                ks += ((double)((tail * KT + gsk - 1) / gsk) + 12.0) / (c.eff_tail > 0 ? c.eff_tail : c.eff);
             }
-            const double t = ks * occ * d.bm * d.bn * (d.bk / 16.0) / c.eff;
+            const double t = ks * occ * d.bm * d.bn * (d.bk / 16.0);
             if (t < best_t * 0.999) {
                 best_t = t;
                 best.id = id;
