@@ -661,23 +661,16 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
     const int total = u1 - u0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool producer = (threadIdx.x == 0);
-    uint64_t pol = 0;
-
-    // producer cursor: k-step, segment end, tile origin
-    int pc_k = u0 - ta * KT, pc_ke = (u1 - ta * KT) < KT ? (u1 - ta * KT) : KT, pc_m0 = 0, pc_n0 = 0;
-    auto pc_tile = [&](int t) {
+    // refills rotate over R warps as in dgemm_tma_kernel; a refill is stateless: local
+    // k-step l of this CTA is tail unit u0 + l, in tile ta or ta + 1 (a range spans <= 2)
+    constexpr int R = 4 < C::CONSUMER_WARPS ? 4 : C::CONSUMER_WARPS;
+    auto issue_at = [&](int slot, int l) {
+        const int u = u0 + l;
+        const int t = u >= (ta + 1) * KT ? ta + 1 : ta;
         int tm, tn;
         tile_coords(hy.tile0 + t, tiles_m, tiles_n, group_m, tm, tn);
-        pc_m0 = tm * C::BM;
-        pc_n0 = tn * C::BN;
-    };
-    auto issue_next = [&](int slot) {
-        tma_issue_stage<C>(base_ptr + slot * C::STAGE_BYTES, &tmA, &tmB, &full[slot], pc_m0, pc_n0, pc_k, pol);
-        if (++pc_k == pc_ke && nseg == 2) {   // second segment: tile ta+1 from k-step 0
-            pc_k = 0;
-            pc_ke = u1 - (ta + 1) * KT;
-            pc_tile(ta + 1);
-        }
+        tma_issue_stage<C>(base_ptr + slot * C::STAGE_BYTES, &tmA, &tmB, &full[slot], tm * C::BM, tn * C::BN,
+                           u - t * KT, l2_policy_evict_normal());
     };
 
     if (producer) {
@@ -689,19 +682,18 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
         fence_mbar_init();
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
-        pol = l2_policy_evict_normal();
-        pc_tile(ta);
     }
     griddep_wait();
     griddep_launch();
     if (producer) {
-        for (int s = 0; s < C::STAGES && s < total; ++s) issue_next(s);
+        for (int s = 0; s < C::STAGES && s < total; ++s) issue_at(s, s);
     }
     __syncthreads();
 
     const int warp_m = warp / C::WARPS_N, warp_n = warp % C::WARPS_N;
     const FragOffsets<C> fo(warp_m, warp_n, lane);
     constexpr int H = 2 * C::KG;
+    constexpr bool kXP = C::E >= 64;   // as in dgemm_tma_kernel: XP pays only for E = 64
     double acc[C::MB][C::NP][2][2];
     int it = 0;
     int stage = 0, phase = 0;
@@ -717,31 +709,40 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
 #pragma unroll
                 for (int jj = 0; jj < 2; ++jj) acc[mb][np][jj][0] = acc[mb][np][jj][1] = 0.0;
         Frag<C> f[2];
-        mbar_wait(&full[stage], (uint32_t)phase);
-        load_half<C>(base + stage * C::STAGE_BYTES, base + stage * C::STAGE_BYTES + C::A_BYTES, 0, fo, f[0]);
+        if constexpr (kXP) {
+            mbar_wait(&full[stage], (uint32_t)phase);
+            load_half<C>(base + stage * C::STAGE_BYTES, base + stage * C::STAGE_BYTES + C::A_BYTES, 0, fo, f[0]);
+        }
         for (int i = 0; i < NK; ++i, ++it) {
-            if (producer && it > 0 && it - 1 + C::STAGES < total) {
+            if (lane == 0 && warp == it % R && it > 0 && it - 1 + C::STAGES < total) {
                 const int sp = stage == 0 ? C::STAGES - 1 : stage - 1;   // slot released at it-1
                 const int pp = stage == 0 ? phase ^ 1 : phase;
                 mbar_wait(&empty[sp], (uint32_t)pp);
-                issue_next(sp);
+                issue_at(sp, it - 1 + C::STAGES);
             }
+            __syncwarp();   // the refilling lane rejoins before the warp-wide mma.sync
             const uint32_t sA = base + stage * C::STAGE_BYTES;
             const int s1 = stage + 1 == C::STAGES ? 0 : stage + 1;
             const int p1 = stage + 1 == C::STAGES ? phase ^ 1 : phase;
+            if constexpr (kXP) {
 #pragma unroll
-            for (int h = 0; h < H; ++h) {
-                if (h + 1 < H) {
-                    load_half<C>(sA, sA + C::A_BYTES, h + 1, fo, f[(h + 1) & 1]);
-                } else {
-                    release_slot(&empty[stage], lane);   // as in dgemm_tma_kernel (XP)
-                    if (i + 1 < NK) {   // cross-stage prefetch inside the segment
-                        mbar_wait(&full[s1], (uint32_t)p1);
-                        const uint32_t sA1 = base + s1 * C::STAGE_BYTES;
-                        load_half<C>(sA1, sA1 + C::A_BYTES, 0, fo, f[0]);
+                for (int h = 0; h < H; ++h) {
+                    if (h + 1 < H) {
+                        load_half<C>(sA, sA + C::A_BYTES, h + 1, fo, f[(h + 1) & 1]);
+                    } else {
+                        release_slot(&empty[stage], lane);   // as in dgemm_tma_kernel (XP)
+                        if (i + 1 < NK) {   // cross-stage prefetch inside the segment
+                            mbar_wait(&full[s1], (uint32_t)p1);
+                            const uint32_t sA1 = base + s1 * C::STAGE_BYTES;
+                            load_half<C>(sA1, sA1 + C::A_BYTES, 0, fo, f[0]);
+                        }
                     }
+                    mma_half<C>(f[h & 1], acc);
                 }
-                mma_half<C>(f[h & 1], acc);
+            } else {
+                mbar_wait(&full[stage], (uint32_t)phase);
+                mma_stage<C>(sA, sA + C::A_BYTES, fo, acc);
+                release_slot(&empty[stage], lane);
             }
             stage = s1;
             phase = p1;

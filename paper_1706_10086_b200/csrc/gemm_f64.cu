@@ -248,7 +248,7 @@ static const Cand k_tma_cands[] = {
     {"tma_256x64x16_w64x32_s4_hybrid", 0.981, 0.966},
     {"tma_64x128x16_w32x64_s4", 0.986},
     {"tma_128x128x16_w32x32_s4", 0.973},       {"tma_64x64x16_w32x16_s6", 0.988},
-    {"tma_64x64x16_w16x32_s6", 0.991},        {"tma_64x64x16_w32x16_s6_hybrid", 0.990, 0.85},
+    {"tma_64x64x16_w16x32_s6", 0.991},        {"tma_64x64x16_w32x16_s6_hybrid", 0.990, 0.88},
     {"tma_64x64x16_w32x16_s6_splitk", 0.992},  {"tma_128x64x16_w32x16_s6_splitk", 0.982},
     {"tma_64x128x16_w32x64_s4_splitk", 0.981}, {"tma_128x128x16_w32x32_s4_splitk", 0.971},
     {"tma_128x64x16_w32x16_s6_streamk", 0.920}, {"tma_64x64x16_w32x16_s6_streamk", 0.852},
