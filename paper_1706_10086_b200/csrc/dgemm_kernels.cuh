@@ -526,24 +526,16 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
     const int u0 = (int)sk_bound(g, U, G), u1 = (int)sk_bound(g + 1, U, G);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool producer = (threadIdx.x == 0);
-    uint64_t pol = 0;
-
-    // producer cursor over global k-steps (incremental: no division per k-step)
-    int pc_tile = u0 / KT;
-    int pc_k = u0 - pc_tile * KT;
-    int pc_m0 = 0, pc_n0 = 0;
-    auto pc_coords = [&]() {
+    // stateless refills rotated over R warps (as in dgemm_tma_kernel): local k-step l is
+    // global unit u0 + l
+    constexpr int R = 4 < C::CONSUMER_WARPS ? 4 : C::CONSUMER_WARPS;
+    auto issue_at = [&](int slot, int l) {
+        const int u = u0 + l;
+        const int t = u / KT;
         int tm, tn;
-        tile_coords(pc_tile, tiles_m, tiles_n, group_m, tm, tn);
-        pc_m0 = tm * C::BM;
-        pc_n0 = tn * C::BN;
-    };
-    auto issue_next = [&](int slot) {   // load the cursor's k-step into ring slot, advance
-        tma_issue_stage<C>(base_ptr + slot * C::STAGE_BYTES, &tmA, &tmB, &full[slot], pc_m0, pc_n0, pc_k, pol);
-        if (++pc_k == KT) {
-            pc_k = 0;
-            if (++pc_tile < tiles_m * tiles_n) pc_coords();
-        }
+        tile_coords(t, tiles_m, tiles_n, group_m, tm, tn);
+        tma_issue_stage<C>(base_ptr + slot * C::STAGE_BYTES, &tmA, &tmB, &full[slot], tm * C::BM, tn * C::BN,
+                           u - t * KT, l2_policy_evict_normal());
     };
     const int nloc = u1 - u0;   // k-steps of this CTA
 
@@ -556,13 +548,11 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
         fence_mbar_init();
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
-        pol = l2_policy_evict_normal();
-        pc_coords();
     }
     griddep_wait();
     griddep_launch();
     if (producer) {
-        for (int s = 0; s < C::STAGES && s < nloc; ++s) issue_next(s);
+        for (int s = 0; s < C::STAGES && s < nloc; ++s) issue_at(s, s);
     }
     __syncthreads();
 
@@ -582,13 +572,14 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
 #pragma unroll
                 for (int j = 0; j < 2; ++j) acc[mb][np][j][0] = acc[mb][np][j][1] = 0.0;
         for (int k = kb; k < ke; ++k, ++li) {
-            if (producer && li > 0 && li - 1 + C::STAGES < nloc) {
+            if (lane == 0 && warp == li % R && li > 0 && li - 1 + C::STAGES < nloc) {
                 // refill the slot released at li-1 (the one before `stage`)
                 const int sp = stage == 0 ? C::STAGES - 1 : stage - 1;
                 const int pp = stage == 0 ? phase ^ 1 : phase;
                 mbar_wait(&empty[sp], (uint32_t)pp);
-                issue_next(sp);
+                issue_at(sp, li - 1 + C::STAGES);
             }
+            __syncwarp();   // the refilling lane rejoins before the warp-wide mma.sync
             mbar_wait(&full[stage], (uint32_t)phase);
             const uint32_t sA = base + stage * C::STAGE_BYTES;
             mma_stage<C>(sA, sA + C::A_BYTES, fo, acc);
