@@ -640,3 +640,23 @@ def test_hybrid_plan_full_size_tail_rows(cuda_lib, shape):
     assert res.ok, f"rows {rows}: {res}"
     del dA, dB, dC
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("cfg_name,splits", [("tma_64x64x16_w32x16_s6_splitk", 2), ("tma_64x64x16_w32x16_s6_splitk", 4),
+                                             ("tma_64x64x16_w32x16_s6", None), ("tma_256x64x16_w64x32_s4_xp", None),
+                                             ("tma_64x64x16_w32x16_s6_hybrid", None),
+                                             ("tma_128x64x16_w32x16_s6_streamk", None)])
+def test_ring_slot_reuse_exact_k_signature(cuda_lib, cfg_name, splits):
+    """Regression for the ring's write-after-read hazard (DESIGN.md §6 "Releasing a slot"):
+    with A = ones and B[k][j] = k + 1, every C entry is exactly K(K+1)/2, and a warp that read
+    a slot after its refill would add STAGES*16 to some k (the error the race produced).
+    Many CTAs, two per SM, every k-step through the ring: 2048^3."""
+    n = 2048
+    A = torch.ones((n, n), dtype=torch.float64, device="cuda")
+    B = torch.arange(1, n + 1, dtype=torch.float64, device="cuda")[:, None].expand(n, n).contiguous()
+    for _ in range(3):
+        C = torch.zeros((n, n), dtype=torch.float64, device="cuda")
+        cuda_lib.gemm(A, B, C, 1.0, 0.0, cfg=cuda_lib.cfg_id(cfg_name), splits=splits)
+        torch.cuda.synchronize()
+        bad = int((C != n * (n + 1) / 2).sum())
+        assert bad == 0, (cfg_name, splits, bad)
