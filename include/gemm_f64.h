@@ -70,6 +70,15 @@ typedef enum {
 
 /* ------------------------------------------------------------------ single GPU */
 
+/* Launch behaviour (all entry points that enqueue GEMM kernels).  Kernels are launched with
+ * programmatic stream serialization (CUDA programmatic dependent launch): a GEMM kernel may
+ * become resident while the previous kernel in the stream is still finishing, but it executes
+ * griddepcontrol.wait -- which returns once that kernel has completed and its memory is
+ * visible -- before its first global-memory access, so stream order is preserved for every
+ * caller.  Setting the environment variable GEMM_PDL=0 (read once per process) launches them
+ * without the attribute.  Calls are capturable into CUDA graphs after one warm-up call on the
+ * stream (workspace and descriptors are created on first use). */
+
 /* C[MxN] = alpha*A[MxK]*B[KxN] + beta*C, row-major, device pointers.
  * Enqueued on the legacy default stream (stream 0, torch's default stream).
  * Returns a gemm_status. */
