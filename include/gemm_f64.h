@@ -148,11 +148,12 @@ typedef struct {
     int bm, bn, bk;     /* CTA tile of C (BM x BN) and k-depth per pipeline stage */
     int wm, wn;         /* warp tile; elements (accumulators) per thread = wm*wn/32 */
     int stages;         /* shared-memory pipeline depth                            */
-    int threads;        /* threads per CTA (lane 0 of warp 0 doubles as TMA producer) */
+    int threads;        /* threads per CTA (TMA refills are issued by lane 0 of warps 0..3 in turn) */
     int smem_bytes;     /* dynamic shared memory per CTA                           */
     int tma;            /* 1: TMA + mbarrier pipeline; 0: cp.async staging          */
     int split_k;        /* 1: no split-K; 0: deterministic split-K, slices chosen per call;
-                           -1: stream-K (persistent grid, even k-step share per CTA)   */
+                           -1: stream-K (persistent grid, even k-step share per CTA);
+                           -2: hybrid (full data-parallel waves + stream-K tail + fix-up) */
     int regs;           /* registers per thread (from cudaFuncGetAttributes; 0 before first use) */
 } gemm_cfg_desc;
 
