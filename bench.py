@@ -417,6 +417,13 @@ def main():
                 "pct_of_fp64_peak": 100.0 * value / (FP64_DATASHEET_TFLOPS * world),
                 "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": a.steps * launches_per_step}
+        if distributed:
+            # the one exchange step: B's broadcast runs on the same stream right
+            # before the GEMM, so its time per step is the step time minus the GEMM's
+            bc = max(0.0, t_ms / a.steps - k_mean)
+            line["exchange"] = {"op": "broadcast of B (NCCL)", "bytes_per_step": 8 * K * N,
+                                "ms_per_step": bc, "share_of_step": bc / (t_ms / a.steps),
+                                "algbw_GBs": (8 * K * N / (bc * 1e-3) / 1e9) if (bc > 0 and world > 1) else None}
         print(json.dumps(line), flush=True)
     if comm is not None:
         comm.close()
