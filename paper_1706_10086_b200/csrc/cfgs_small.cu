@@ -24,6 +24,9 @@ static const CfgEntry k_table[] = {
     DG_SK(64, 64, 16, 32, 16, 6),
     DG_SK(128, 64, 16, 32, 16, 6),
     DG_HYB(64, 64, 16, 32, 16, 6),
+    DG_TMA(64, 64, 32, 16, 32, 3),
+    DG_TMA_SPLIT(64, 64, 32, 32, 16, 3),
+    DG_HYB(64, 64, 32, 32, 16, 3),
 };
 
 const CfgEntry *cfg_table_small(int *n) {

@@ -243,12 +243,15 @@ struct Cand {
     double eff_tail = 0.0;   // hybrid: efficiency of its stream-K tail kernel (0: same as eff)
 };
 static const Cand k_tma_cands[] = {
-    // eff = measured fraction of the clock roof at 16384^3 (profiles/r01_f2_tuner_table_run_v7.log)
+    // eff = measured fraction of the clock roof at 16384^3 (profiles/r01_f2_tuner_table_run_v7.log, _v11.log)
     {"tma_256x64x16_w64x32_s4_xp", 0.979},     {"tma_128x128x16_w64x32_s4_xp", 0.980},
     {"tma_256x64x16_w64x32_s4_hybrid", 0.981, 0.966},
     {"tma_64x128x16_w32x64_s4", 0.986},
     {"tma_128x128x16_w32x32_s4", 0.973},       {"tma_64x64x16_w32x16_s6", 0.988},
     {"tma_64x64x16_w16x32_s6", 0.991},        {"tma_64x64x16_w32x16_s6_hybrid", 0.990, 0.88},
+    // BK = 32, 3 stages: half the barrier and refill work per FLOP (table v11)
+    {"tma_64x64x32_w16x32_s3", 0.990},        {"tma_64x64x32_w32x16_s3_splitk", 0.994},
+    {"tma_64x64x32_w32x16_s3_hybrid", 0.993, 0.88},
     {"tma_64x64x16_w32x16_s6_splitk", 0.992},  {"tma_128x64x16_w32x16_s6_splitk", 0.982},
     {"tma_64x128x16_w32x64_s4_splitk", 0.981}, {"tma_128x128x16_w32x32_s4_splitk", 0.971},
     {"tma_128x64x16_w32x16_s6_streamk", 0.920}, {"tma_64x64x16_w32x16_s6_streamk", 0.852},
