@@ -527,21 +527,18 @@ int validate(int64_t M, int64_t N, int64_t K, double alpha, const double *A, int
 }
 
 // Grouped raster (a1): consecutive CTAs walk group_m tile-rows column by column, so the
-// CTAs resident at one time cover about group_m x (G / group_m) tiles (G = SMs x CTAs per
-// SM) and share their A row panels and B column panels in L2 at each k-step.  The region's
-// k-slice bytes, 8*BK*(group_m*BM + (G/group_m)*BN), are smallest for a region that is
-// square in elements: group_m = sqrt(G*BN/BM) (8 for 256x64 tiles at 1 CTA/SM, 17 for
-// 64x64 at 2).  GEMM_GROUP_M overrides it (measurements).
-static int raster_group(const gemm_cfg_desc &d, int occ, int64_t M) {
+// CTAs resident at one time share their A row panels and B column panels in L2 at each
+// k-step.  group_m = 8 for every configuration: swept for the bench kernel (64x64 tiles,
+// BK=32, two CTAs per SM) it gives the fewest DRAM bytes (110 GB per 16384^3 GEMM against
+// 123-484 GB for 4, 6, 12, 17, 32, 64) at the same speed (+-0.05 %, the kernel is
+// compute-bound; profiles/r01_group_m_sweep.txt).  GEMM_GROUP_M overrides it (measurements).
+static int raster_group(const gemm_cfg_desc &, int, int64_t M) {
     static const int forced = [] {
         const char *e = std::getenv("GEMM_GROUP_M");
         return e ? std::atoi(e) : 0;
     }();
-    if (forced > 0) return forced;
-    const double G = (double)num_sms() * (occ > 0 ? occ : 1);
-    int g = (int)std::lround(std::sqrt(G * d.bn / d.bm));
-    const int64_t tiles_m = (M + d.bm - 1) / d.bm;
-    return (int)std::max<int64_t>(1, std::min<int64_t>(g, std::max<int64_t>(1, tiles_m)));
+    const int g = forced > 0 ? forced : 8;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(g, M));
 }
 
 int gemm_impl(int64_t M, int64_t N, int64_t K, double alpha, const double *A, int64_t lda, const double *B,

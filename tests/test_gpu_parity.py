@@ -643,6 +643,7 @@ def test_hybrid_plan_full_size_tail_rows(cuda_lib, shape):
 
 
 @pytest.mark.parametrize("cfg_name,splits", [("tma_64x64x16_w32x16_s6_splitk", 2), ("tma_64x64x16_w32x16_s6_splitk", 4),
+                                             ("tma_64x64x32_w32x16_s3_splitk", 4), ("tma_64x64x32_w32x16_s3_hybrid", None),
                                              ("tma_64x64x16_w32x16_s6", None), ("tma_256x64x16_w64x32_s4_xp", None),
                                              ("tma_64x64x16_w32x16_s6_hybrid", None),
                                              ("tma_128x64x16_w32x16_s6_streamk", None)])
