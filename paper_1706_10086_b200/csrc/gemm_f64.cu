@@ -268,7 +268,10 @@ static double est_time(const gemm_cfg_desc &d, int occ, int sms, int64_t M, int6
     const int64_t KT = (K + d.bk - 1) / d.bk;
     const int64_t slots = (int64_t)sms * occ;
     const int64_t waves = (tiles * S + slots - 1) / slots;
-    const double ksteps = (double)((KT + S - 1) / S) + 4.0 + (S > 1 ? 2.0 : 0.0);
+    // fixed costs are counted in 16-deep k-steps (pipeline fill, epilogue, split reduction),
+    // so a BK = 32 stage is charged half as many of its own steps
+    const double u = 16.0 / d.bk;
+    const double ksteps = (double)((KT + S - 1) / S) + (4.0 + (S > 1 ? 2.0 : 0.0)) * u;
     return (double)waves * occ * d.bm * d.bn * ksteps * (d.bk / 16.0) / eff;
 }
 
@@ -340,10 +343,11 @@ static Choice choose_uncached(int64_t M, int64_t N, int64_t K, bool tma, bool si
             // the full waves run at the data-parallel kernel's efficiency, the tail at its
             // stream-K kernel's (lower for the E=16 warp tiles: without it the model sent
             // skinny and K-heavy shapes to the 64x64 hybrid, 6-12 % slower than the best)
-            double ks = (double)W * (double)(KT + 4) / c.eff;
+            const double u = 16.0 / d.bk;   // fixed costs in 16-deep k-steps (see est_time)
+            double ks = (double)W * ((double)KT + 4.0 * u) / c.eff;
             if (tail > 0) {   // + pipeline fill, partial store, fix-up and two launch gaps
                 const int64_t gsk = std::min<int64_t>(G, std::max<int64_t>(tail, tail * KT / 16));
-                ks += ((double)((tail * KT + gsk - 1) / gsk) + 12.0) / (c.eff_tail > 0 ? c.eff_tail : c.eff);
+                ks += ((double)((tail * KT + gsk - 1) / gsk) + 12.0 * u) / (c.eff_tail > 0 ? c.eff_tail : c.eff);
             }
             const double t = ks * occ * d.bm * d.bn * (d.bk / 16.0);
             if (t < best_t * 0.999) {
@@ -361,7 +365,8 @@ static Choice choose_uncached(int64_t M, int64_t N, int64_t K, bool tma, bool si
             const int64_t tiles = ((M + d.bm - 1) / d.bm) * ((N + d.bn - 1) / d.bn);
             const int64_t G = std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * occ, tiles * KT));
             const double per_cta_tiles = (double)((tiles + G - 1) / G) + 1.0;
-            const double t = ((double)((tiles * KT + G - 1) / G) + 4.0 * per_cta_tiles + 6.0) * occ * d.bm * d.bn *
+            const double t = ((double)((tiles * KT + G - 1) / G) + (4.0 * per_cta_tiles + 6.0) * 16.0 / d.bk) * occ *
+                             d.bm * d.bn *
                              (d.bk / 16.0) / c.eff;
             if (t < best_t * 0.999) {
                 best_t = t;
