@@ -266,13 +266,19 @@ static double est_time(const gemm_cfg_desc &d, int occ, int sms, int64_t M, int6
                        double eff) {
     const int64_t tiles = ((M + d.bm - 1) / d.bm) * ((N + d.bn - 1) / d.bn);
     const int64_t KT = (K + d.bk - 1) / d.bk;
-    const int64_t slots = (int64_t)sms * occ;
-    const int64_t waves = (tiles * S + slots - 1) / slots;
+    // quantised per SM, not per CTA slot: the CTAs an SM holds share its DMMA pipe, so an SM
+    // that ends with one CTA instead of two finishes it in about half the time (with
+    // ceil(CTAs / (SMs x occupancy)) full slot-waves the model over-charged short split-K
+    // waves of the two-CTA-per-SM tiles by up to 9 %, r01_heuristic_regret_v5_*.csv)
+    // ... but a CTA of a two-per-SM tile that is alone on its SM runs at only ~60 % of the SM's
+    // DMMA rate, so a grid that cannot give any SM a second CTA is charged for that.
+    const int64_t per_sm = (tiles * S + sms - 1) / sms;
+    const double lone = (occ > 1 && tiles * S <= sms) ? 1.0 / 0.6 : 1.0;
     // fixed costs are counted in 16-deep k-steps (pipeline fill, epilogue, split reduction),
     // so a BK = 32 stage is charged half as many of its own steps
     const double u = 16.0 / d.bk;
     const double ksteps = (double)((KT + S - 1) / S) + (4.0 + (S > 1 ? 2.0 : 0.0)) * u;
-    return (double)waves * occ * d.bm * d.bn * ksteps * (d.bk / 16.0) / eff;
+    return (double)per_sm * lone * d.bm * d.bn * ksteps * (d.bk / 16.0) / eff;
 }
 
 static Choice choose_uncached(int64_t M, int64_t N, int64_t K, bool tma, bool single_pass);
