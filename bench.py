@@ -380,6 +380,9 @@ def main():
                 "frac": achieved / FP64_DATASHEET_TFLOPS, "traffic": traffic,
                 "kernel": cfg_name, "kernel_ms_mean": k_mean, "flops_per_launch": flops_local,
                 "launches_per_gemm": launches_per_step,
+                # compulsory HBM bytes of one GEMM (A, B read once, C written once; beta = 0), for
+                # comparison with `traffic` (DESIGN.md §6 explains the gap: L2-sized waves)
+                "algorithmic_bytes": 8.0 * (Ml * K + K * N + Ml * N),
                 "peak_source": "FP64 / FP64-tensor datasheet peak of one HGX B200 GPU (296/8); MEASURED_PEAKS.json has "
                                "no FP64 entry (DESIGN.md §Roofline)"}
     if peaks.get("bf16_tflops"):
