@@ -341,7 +341,9 @@ static Choice choose_uncached(int64_t M, int64_t N, int64_t K, bool tma, bool si
         }
         const gemm_cfg_desc &d = g_cfgs[id].d;
         const int64_t KT = (K + d.bk - 1) / d.bk;
-        if (single_pass && d.split_k != 1) continue;
+        // one k-pass per tile: plain configurations, and split-K instances run with one slice
+        // (the same per-entry chain; test_all_cfgs_bitwise_identical_and_deterministic)
+        if (single_pass && d.split_k < 0) continue;
         if (d.split_k == -2) {   // hybrid: W full waves + the tail's k-steps spread over gsk CTAs
             const int64_t tiles = ((M + d.bm - 1) / d.bm) * ((N + d.bn - 1) / d.bn);
             const int64_t G = (int64_t)sms * occ;
@@ -381,7 +383,7 @@ static Choice choose_uncached(int64_t M, int64_t N, int64_t K, bool tma, bool si
             }
             continue;
         }
-        const int smax = d.split_k == 1 ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(16, KT / 2));
+        const int smax = (d.split_k == 1 || single_pass) ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(16, KT / 2));
         for (int S = 1; S <= smax; ++S) {
             const double t = est_time(d, occ, sms, M, N, K, S, c.eff);
             if (t < best_t * 0.999) {
