@@ -1,0 +1,38 @@
+// launch.cuh -- kernel launch with programmatic dependent launch (PDL), shared by the FP64
+// and FP32 translation units.
+#pragma once
+#include <cstdlib>
+#include <cuda_runtime.h>
+#include <utility>
+
+namespace dg {
+
+// Every GEMM kernel is launched with programmatic stream serialization (PDL): it may become
+// resident while the previous kernel of the stream drains and waits for it in-kernel
+// (griddep_wait in ptx.cuh) before touching global memory.  GEMM_PDL=0 in the environment
+// launches them the classic way (A/B measurements).
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char *e = std::getenv("GEMM_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+}  // namespace dg

@@ -32,6 +32,7 @@
 #include "dgemm_kernels.cuh"
 #include "internal.h"
 #include "ptx.cuh"
+#include "launch.cuh"
 
 namespace dg {
 
@@ -164,6 +165,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    griddep_wait();     // PDL: setup above overlapped the previous kernel; memory from here on
+    griddep_launch();
 
     if (warp == 0) {
         if (lane == 0) {   // ---------------- TMA producer
@@ -370,6 +373,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C::THREADS, 1)
     cluster_sync_all();   // both CTAs: barriers initialised, TMEM allocated
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    griddep_wait();     // PDL: setup above overlapped the previous kernel; memory from here on
+    griddep_launch();
 
     if (warp == 0) {
         if (lane == 0) {   // ---------------- TMA producer (both CTAs)
@@ -460,6 +465,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C::THREADS, 1)
 // x -> (rn_tf32(x), rn_tf32(x - rn_tf32(x))), packed rows of pitch ldo.
 __global__ void split_tf32_kernel(const float *__restrict__ X, int64_t ldx, int64_t rows, int64_t cols,
                                   float *__restrict__ hi, float *__restrict__ lo, int64_t ldo) {
+    griddep_wait();
+    griddep_launch();
     const int64_t total = rows * cols;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
          idx += (int64_t)gridDim.x * blockDim.x) {
@@ -479,6 +486,8 @@ __global__ void split_tf32_kernel(const float *__restrict__ X, int64_t ldx, int6
 __global__ void split_tf32_t_kernel(const float *__restrict__ X, int64_t ldx, int64_t rows, int64_t cols,
                                     float *__restrict__ hiT, float *__restrict__ loT, int64_t ldo) {
     __shared__ float tile[32][33];
+    griddep_wait();
+    griddep_launch();
     const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
     const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
 #pragma unroll
@@ -503,6 +512,8 @@ __global__ void split_tf32_t_kernel(const float *__restrict__ X, int64_t ldx, in
 }
 
 __global__ void scale_f32_kernel(int M, int N, float beta, float *__restrict__ Cm, int64_t ldc) {
+    griddep_wait();
+    griddep_launch();
     const int64_t total = (int64_t)M * N;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
          idx += (int64_t)gridDim.x * blockDim.x) {
@@ -526,8 +537,8 @@ template <class C>
 static void launch_f32(dim3 grid, cudaStream_t st, const CUtensorMap &a, const CUtensorMap &b, const CUtensorMap &c,
                        const CUtensorMap &d, int M, int N, int K, float alpha, float beta, float *Cm, int64_t ldc,
                        int group_m) {
-    sgemm_3xtf32_kernel<C><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(a, b, c, d, M, N, K, alpha, beta, Cm, ldc,
-                                                                     group_m);
+    (void)launch_k(sgemm_3xtf32_kernel<C>, grid, dim3(C::THREADS), C::SMEM_BYTES, st, a, b, c, d, M, N, K, alpha,
+                   beta, Cm, ldc, group_m);   // errors surface through cudaGetLastError at the call site
 }
 
 #define F32CFG(BN, BK, ST)                                                                                   \
@@ -538,8 +549,8 @@ template <class C>
 static void launch_f32_pair(dim3 grid, cudaStream_t st, const CUtensorMap &a, const CUtensorMap &b,
                             const CUtensorMap &c, const CUtensorMap &d, int M, int N, int K, float alpha, float beta,
                             float *Cm, int64_t ldc, int group_m) {
-    sgemm_3xtf32_2sm_kernel<C><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(a, b, c, d, M, N, K, alpha, beta, Cm, ldc,
-                                                                         group_m);
+    (void)launch_k(sgemm_3xtf32_2sm_kernel<C>, grid, dim3(C::THREADS), C::SMEM_BYTES, st, a, b, c, d, M, N, K,
+                   alpha, beta, Cm, ldc, group_m);
 }
 
 // pair configurations: bm = 256 (two CTAs), the A box is 128 rows, the B box BN/2 rows
@@ -619,8 +630,8 @@ static int impl(int64_t M, int64_t N, int64_t K, float alpha, const float *A, in
         if (beta == 1.0f) return GEMM_OK;
         const int64_t total = M * N;
         const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-        scale_f32_kernel<<<blocks, 256, 0, st>>>((int)M, (int)N, beta, C, ldc);
-        return cuda_check(cudaGetLastError(), "scale_f32_kernel launch");
+        return cuda_check(launch_k(scale_f32_kernel, dim3(blocks), dim3(256), 0, st, (int)M, (int)N, beta, C, ldc),
+                          "scale_f32_kernel launch");
     }
     if (cfg_id < -1 || cfg_id >= kNumF32Cfgs)
         return set_error(GEMM_ERR_ARG, "f32 cfg_id=%d out of range [-1, %d)", cfg_id, kNumF32Cfgs);
@@ -636,11 +647,14 @@ static int impl(int64_t M, int64_t N, int64_t K, float alpha, const float *A, in
     float *Ah = ws, *Al = Ah + a_sz, *Bh = Al + a_sz, *Bl = Bh + b_sz;
     {
         const int64_t ta = M * K, tb = K * N;
-        split_tf32_kernel<<<(int)std::min<int64_t>((ta + 255) / 256, 148 * 32), 256, 0, st>>>(A, lda, M, K, Ah, Al, ka);
+        int rc = cuda_check(launch_k(split_tf32_kernel, dim3((unsigned)std::min<int64_t>((ta + 255) / 256, 148 * 32)),
+                                     dim3(256), 0, st, A, lda, M, K, Ah, Al, ka),
+                            "split_tf32_kernel launch");
+        if (rc) return rc;
         (void)tb;
         dim3 tgrid((unsigned)((N + 31) / 32), (unsigned)((K + 31) / 32));
-        split_tf32_t_kernel<<<tgrid, dim3(32, 8), 0, st>>>(B, ldb, K, N, Bh, Bl, ka);
-        int rc = cuda_check(cudaGetLastError(), "split_tf32_kernel launch");
+        rc = cuda_check(launch_k(split_tf32_t_kernel, tgrid, dim3(32, 8), 0, st, B, ldb, K, N, Bh, Bl, ka),
+                        "split_tf32_t_kernel launch");
         if (rc) return rc;
     }
     CUtensorMap mAh, mAl, mBh, mBl;
