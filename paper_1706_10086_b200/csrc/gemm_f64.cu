@@ -251,7 +251,7 @@ static const Cand k_tma_cands[] = {
     {"tma_64x64x16_w16x32_s6", 0.991},        {"tma_64x64x16_w32x16_s6_hybrid", 0.990, 0.88},
     // BK = 32, 3 stages: half the barrier and refill work per FLOP (table v11)
     {"tma_64x64x32_w16x32_s3", 0.990},        {"tma_64x64x32_w32x16_s3_splitk", 0.994},
-    {"tma_64x64x32_w32x16_s3_hybrid", 0.993, 0.88},
+    {"tma_64x64x32_w32x16_s3_hybrid", 0.993, 0.95},
     {"tma_64x64x16_w32x16_s6_splitk", 0.992},  {"tma_128x64x16_w32x16_s6_splitk", 0.982},
     {"tma_64x128x16_w32x64_s4_splitk", 0.981}, {"tma_128x128x16_w32x32_s4_splitk", 0.971},
     {"tma_128x64x16_w32x16_s6_streamk", 0.920}, {"tma_64x64x16_w32x16_s6_streamk", 0.852},
