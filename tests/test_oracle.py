@@ -243,6 +243,85 @@ def test_checker_rejects_nan():
     assert not r.ok and r.n_nan == 1
 
 
+def _beta_heavy_case(seed=41):
+    """alpha=1.5, beta=0.5 with |C0| ~ 1e6 and |A||B| ~ 1e-6: the beta term dominates."""
+    rng = np.random.default_rng(seed)
+    A = rng.uniform(-1, 1, (24, 48)) * 1e-3
+    B = rng.uniform(-1, 1, (48, 20)) * 1e-3
+    C0 = rng.uniform(0.5, 1.0, (24, 20)) * 1e6 * rng.choice([-1.0, 1.0], (24, 20))
+    C, mag = oracle.dgemm(1.5, A, B, 0.5, C0, want_mag=True)
+    return A, B, C0, C, mag
+
+
+def test_bound_beta_term_rejects_error_far_above_rounding_of_beta_c0():
+    """Fault injection at alpha=1.5, beta=0.5 (config 3): an error delta with
+    u|beta||C0| << delta << |C0| must fail.  Here u|beta||C0| ~ 5e-11 and delta = 1e-4 while
+    |C0| ~ 1e6: a bound whose beta term lost its u (4|beta||C0| ~ 2e6) would accept it."""
+    A, B, C0, C, mag = _beta_heavy_case()
+    bnd = oracle.bound(48, 1.5, 0.5, mag, C0)
+    bad = C.copy()
+    bad[3, 4] += 1e-4
+    r = oracle.check(bad, C, bnd)
+    assert not r.ok and r.worst == (3, 4) and r.n_bad == 1
+    # ... and the unperturbed result, plus a last-bit flip of one entry, still pass
+    assert oracle.check(C, C, bnd).ok
+    flip = C.copy()
+    flip[3, 4] = np.nextafter(flip[3, 4], np.inf)
+    assert oracle.check(flip, C, bnd).ok
+
+
+def test_bound_with_zero_a_is_the_beta_term_exactly():
+    """A = 0 makes mag = 0, so the bound reduces to its beta term: 4 u |beta| |C0| + 1e-300
+    (u = 2^-53, a power of two, so the expected value is computed exactly)."""
+    _, B, C0, _, _ = _beta_heavy_case(seed=42)
+    A = np.zeros((24, 48))
+    C, mag = oracle.dgemm(1.5, A, B, 0.5, C0, want_mag=True)
+    assert np.all(mag == 0.0)
+    expect = (np.abs(C0) * 0.5) * 2.0 ** -51 + 1e-300
+    assert np.array_equal(oracle.bound(48, 1.5, 0.5, mag, C0), expect)
+    assert np.array_equal(C, 0.5 * C0)   # beta*C0, exact (power-of-two scale)
+
+
+@pytest.mark.parametrize("ab", [(1.5, 0.5), (-3.0, 2.0), (1.0, 0.0), (0.25, -8.0)])
+def test_bound_is_bracketed_by_exact_rational_error(ab):
+    """Two-sided pin of the whole bound against exact rational arithmetic (Fraction), at
+    several alpha/beta: (lower) it is at least the oracle's true error, so a correct result
+    never fails; (upper) it is at most 8x the textbook worst case gamma_K|alpha|mag +
+    3u|beta||C0| + 2u|exact| (gamma_K = Ku/(1-Ku)), so a term that lost its u, a wrong K
+    factor or a beta term scaled by something other than |beta| makes it too loose."""
+    alpha, beta = ab
+    rng = np.random.default_rng(7)
+    M, N, K = 5, 6, 7
+    A = rng.uniform(-1, 1, (M, K)) * 10.0 ** rng.integers(-2, 3, (M, K))
+    B = rng.uniform(-1, 1, (K, N)) * 10.0 ** rng.integers(-2, 3, (K, N))
+    C0 = rng.uniform(-1, 1, (M, N)) * 10.0 ** rng.integers(-2, 6, (M, N))
+    got, mag = oracle.dgemm(alpha, A, B, beta, C0, want_mag=True)
+    bnd = oracle.bound(K, alpha, beta, mag, C0)
+    ex, exmag = _exact(alpha, A, B, beta, C0)
+    u = Fraction(1, 2 ** 53)
+    gam = K * u / (1 - K * u)
+    for i in range(M):
+        for j in range(N):
+            err = abs(Fraction(got[i, j]) - ex[i][j])
+            assert Fraction(bnd[i, j]) >= err, (i, j)
+            worst = gam * abs(Fraction(alpha)) * exmag[i][j] + 3 * u * abs(Fraction(beta) * Fraction(C0[i, j])) \
+                + 2 * u * abs(ex[i][j])
+            assert Fraction(bnd[i, j]) <= 8 * worst + Fraction(1e-300), (i, j, float(bnd[i, j]), float(worst))
+
+
+def test_bound_f32_beta_term_pins():
+    """bound_f32 at alpha=1.5, beta=0.5 with mag = 0: exactly 4 u32 |beta||C0| + 1e-30
+    (u32 = 2^-23), i.e. 2^-22 |C0| in [0.12, 0.24] for |C0| in [5e5, 1e6].  An error of 1.0
+    fails and one of 0.0125 passes; a beta term that lost its u32 (~1e6) would pass both."""
+    _, B, C0, _, _ = _beta_heavy_case(seed=43)
+    mag = np.zeros_like(C0)
+    b = oracle.bound_f32(48, 1.5, 0.5, mag, C0)
+    assert np.array_equal(b, (np.abs(C0) * 0.5) * 2.0 ** -21 + 1e-30)   # 4 u32 = 2^-21
+    ref = 0.5 * C0
+    assert not oracle.check(ref + 1.0, ref, b).ok
+    assert oracle.check(ref + 0.0125, ref, b).ok
+
+
 def test_bound_is_tight_enough_to_catch_a_dropped_term():
     """Dropping one k term must exceed the bound (the bound is not vacuous)."""
     A, B, C0 = synth.problem(16, 16, 256, seed=12)
