@@ -76,8 +76,16 @@ typedef enum {
  * griddepcontrol.wait -- which returns once that kernel has completed and its memory is
  * visible -- before its first global-memory access, so stream order is preserved for every
  * caller.  Setting the environment variable GEMM_PDL=0 (read once per process) launches them
- * without the attribute.  Calls are capturable into CUDA graphs after one warm-up call on the
- * stream (workspace and descriptors are created on first use). */
+ * without the attribute.
+ *
+ * Workspace and CUDA graphs.  Split-K / stream-K partials, tile counters and repack buffers
+ * are library workspace cached per (device, stream) and created on first use.  Calls are
+ * capturable into CUDA graphs after one eager warm-up call of the largest shape on the
+ * capture stream (an allocation during capture fails with GEMM_ERR_ALLOC).  Workspace that a
+ * call used is never freed while the process runs unless gemm_workspace_release() is called:
+ * when a later call needs more, the old buffer is retired (kept) and a larger one allocated,
+ * so a captured graph stays valid.  A graph replays on its capture stream's workspace: do
+ * not replay it concurrently with eager calls on that stream, or with itself. */
 
 /* C[MxN] = alpha*A[MxK]*B[KxN] + beta*C, row-major, device pointers.
  * Enqueued on the legacy default stream (stream 0, torch's default stream).
@@ -103,7 +111,9 @@ GEMM_API int gemm_f64_cfg(int64_t M, int64_t N, int64_t K, double alpha,
 /* Same as gemm_f64_cfg, additionally forcing the number of deterministic split-K
  * slices for a *_splitk configuration (splits = 0: the model's choice; 1: no
  * split).  Forcing splits > 1 on a configuration without split-K returns
- * GEMM_ERR_UNSUPPORTED. */
+ * GEMM_ERR_UNSUPPORTED.  With cfg_id = -1: splits = 0 is gemm_f64_cfg(-1); splits = 1
+ * restricts the heuristic to one k-pass per tile (no split-K / stream-K); splits > 1
+ * restricts it to the *_splitk configurations and launches exactly `splits` slices. */
 GEMM_API int gemm_f64_ex(int64_t M, int64_t N, int64_t K, double alpha,
                 const double *A, int64_t lda, const double *B, int64_t ldb,
                 double beta, double *C, int64_t ldc, int cfg_id, int splits, void *cuda_stream);
@@ -141,6 +151,12 @@ GEMM_API int gemm_f64_host(int64_t M, int64_t N, int64_t K, double alpha,
 
 /* Release the device buffers cached by gemm_f64_host on the current device. */
 GEMM_API int gemm_host_pool_release(void);
+
+/* Synchronizes the current device, then frees every workspace buffer the device entry points
+ * cached on it (FP64 split-K / stream-K partials and counters, repack buffers, FP32 split
+ * workspace), retired ones included.  CUDA graphs captured from earlier calls must not be
+ * replayed afterwards. */
+GEMM_API int gemm_workspace_release(void);
 
 /* ------------------------------------------------------------ configurations */
 
@@ -209,12 +225,24 @@ GEMM_API int gemm_peak_probe(int kind, int blocks, int warps, int64_t iters,
 
 /* --------------------------------------------------- multi-GPU (one process per GPU) */
 
-/* Rank 0 creates the 128-byte NCCL unique id; distribute it to all ranks
- * (e.g. with torch.distributed.broadcast) before gemm_comm_init. */
+/* The paper computes on one device and has no communication ("Alpaka does not abstract the
+ * inter-node communication", §1.2); the multi-GPU split below is the north star's
+ * (BASELINE.json: "C is partitioned by row blocks: A is row-sharded, B is broadcast over
+ * NVLink with NCCL"), SURVEY.md §8(b)/(e).  Errors follow SPEC's "dimension/tile mismatch ->
+ * error" and "error naming n, t, e": a non-OK code plus gemm_last_error().
+ *
+ * Rank 0 creates the 128-byte NCCL unique id (id_out: caller-owned 128 bytes; NCCL failure ->
+ * GEMM_ERR_NCCL); distribute it to all ranks (e.g. with torch.distributed.broadcast) before
+ * gemm_comm_init. */
 GEMM_API int gemm_comm_unique_id(unsigned char id_out[128]);
-/* Creates the library-owned communicator for `rank` of `nranks` on the current
- * device.  *comm_out receives an opaque handle. */
+/* Creates the library-owned communicator for `rank` of `nranks` on the current device
+ * (collective over the nranks processes).  *comm_out receives an opaque handle owned by the
+ * library (a private NCCL communicator, a communication stream, events and the column-panel
+ * workspace), released by gemm_comm_destroy.  Bad rank / nranks / NULL -> GEMM_ERR_ARG;
+ * NCCL failure -> GEMM_ERR_NCCL (nothing is left allocated). */
 GEMM_API int gemm_comm_init(void **comm_out, int nranks, const unsigned char id[128], int rank);
+/* Destroys a communicator (NULL is a no-op).  Collective like ncclCommDestroy; the caller
+ * must have synchronized the streams its calls used. */
 GEMM_API int gemm_comm_destroy(void *comm);
 
 /* Row-block-sharded GEMM (collective: every rank calls it with the same N, K,
@@ -225,14 +253,21 @@ GEMM_API int gemm_comm_destroy(void *comm);
  * NCCL, in `bcast_chunks` column panels (>= 1) so that panel j+1 travels while
  * panel j is multiplied -- per-entry arithmetic is unchanged, so the result is
  * bitwise equal to the single-GPU call with the same configuration.
- * Then each rank computes C_local = alpha*A_local*B + beta*C_local. */
+ * Then each rank computes C_local = alpha*A_local*B + beta*C_local (Eq. (1) P:77-79 on its
+ * rows).  `bcast_chunks` extends SURVEY §8(b)'s signature with §8(e)'s overlap option
+ * ("N-panel chunking"): 1 = one broadcast of B, then the local GEMM; c > 1 = c column panels
+ * (widths multiples of 16, at most N/64 panels).  The library's column-panel workspace is
+ * reused by the next call only after this call's GEMMs finished (stream-ordered), whatever
+ * stream either call uses.  Asynchronous on `cuda_stream`; argument errors as gemm_f64 ->
+ * nothing enqueued; NCCL errors -> GEMM_ERR_NCCL. */
 GEMM_API int gemm_f64_sharded(int64_t M_local, int64_t N, int64_t K, double alpha,
                      const double *A_local, int64_t lda, double *B, int64_t ldb,
                      double beta, double *C_local, int64_t ldc,
                      void *comm, int root, int bcast_chunks, void *cuda_stream);
 
-/* Plain broadcast of a device buffer of `count` doubles (exposed for tests and
- * for timing the exchange step alone). */
+/* Plain broadcast of a device buffer of `count` doubles from `root` (in place, ncclBroadcast;
+ * the one exchange step of SURVEY §8(e), exposed for tests and for timing it alone).
+ * count < 0, bad root or NULL -> GEMM_ERR_ARG; NCCL failure -> GEMM_ERR_NCCL. */
 GEMM_API int gemm_bcast_f64(double *buf, int64_t count, int root, void *comm, void *cuda_stream);
 
 /* Library version string. */

@@ -1,10 +1,13 @@
 """Build libgemm_f64.so in-tree for sm_100a (nvcc; no torch extension machinery).
 
-    python -m paper_1706_10086_b200.build [--force]
+    python -m paper_1706_10086_b200.build [--force] [--trace]
 
 Compiles every csrc/*.cu with `-gencode arch=compute_100a,code=sm_100a -O3
 -lineinfo` (no fast-math), links the static CUDA runtime and the NCCL shipped
 with torch (nvidia/nccl), and writes paper_1706_10086_b200/libgemm_f64.so.
+
+--trace builds an instrumented copy (-DDG_TRACE: per-CTA globaltimer timeline, see
+csrc/ptx.cuh) as libgemm_f64_trace.so for tools/trace_ctas.py; the product never loads it.
 """
 
 from __future__ import annotations
@@ -20,6 +23,8 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libgemm_f64.so")
 BUILD = os.path.join(HERE, "build")
+TRACE_LIB = os.path.join(HERE, "libgemm_f64_trace.so")
+TRACE_BUILD = os.path.join(HERE, "build_trace")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -50,24 +55,25 @@ def _deps():
         glob.glob(os.path.join(CSRC, "*.inc")) + [os.path.join(ROOT, "include", "gemm_f64.h"), __file__]
 
 
-def up_to_date() -> bool:
-    if not os.path.exists(LIB):
+def up_to_date(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return False
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return all(os.path.getmtime(d) <= t for d in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
-        return LIB
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    lib_out, build_dir = (TRACE_LIB, TRACE_BUILD) if trace else (LIB, BUILD)
+    if not force and up_to_date(lib_out):
+        return lib_out
+    os.makedirs(build_dir, exist_ok=True)
     nccl_inc, nccl_lib = _nccl_dirs()
     nvcc = _nvcc()
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-Xptxas", "-v",
-                    "-I", os.path.join(ROOT, "include"), "-I", nccl_inc]
+                    "-I", os.path.join(ROOT, "include"), "-I", nccl_inc] + (["-DDG_TRACE"] if trace else [])
 
     def compile_one(src):
-        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+        obj = os.path.join(build_dir, os.path.basename(src) + ".o")
         cmd = [nvcc] + flags + ["-c", src, "-o", obj]
         p = subprocess.run(cmd, capture_output=True, text=True)
         if p.returncode != 0:
@@ -79,17 +85,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(compile_one, sources()))
     nccl_so = sorted(glob.glob(os.path.join(nccl_lib, "libnccl.so*")))[0]
-    tmp = LIB + ".tmp"
+    tmp = lib_out + ".tmp"
     cmd = [nvcc] + ARCH + ["-shared", "-cudart", "static", "-o", tmp] + objs + \
         ["-Xlinker", nccl_so, "-Xlinker", "-rpath=" + nccl_lib, "-lpthread", "-ldl", "-lrt"]
     p = subprocess.run(cmd, capture_output=True, text=True)
     if p.returncode != 0:
         raise RuntimeError(f"link failed:\n{p.stderr}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib_out)
     if verbose:
-        print(f"built {LIB}")
-    return LIB
+        print(f"built {lib_out}")
+    return lib_out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    build(force="--force" in sys.argv, verbose=True, trace="--trace" in sys.argv)

@@ -27,6 +27,11 @@ static const CfgEntry k_table[] = {
     DG_TMA(64, 64, 32, 16, 32, 3),
     DG_TMA_SPLIT(64, 64, 32, 32, 16, 3),
     DG_HYB(64, 64, 32, 32, 16, 3),
+    // round 2: BK = 32 stream-K (small shapes whose operands stay in L2) and E = 32 tiles
+    DG_SK(64, 64, 32, 32, 16, 3),
+    DG_SK(64, 64, 32, 16, 32, 3),
+    DG_SK(128, 64, 32, 32, 32, 3),
+    DG_TMA_SPLIT(128, 64, 32, 32, 32, 3),
 };
 
 const CfgEntry *cfg_table_small(int *n) {

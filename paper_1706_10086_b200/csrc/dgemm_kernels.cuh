@@ -272,6 +272,52 @@ __device__ __forceinline__ double *partial_slot(double *ws, int64_t slot, int wa
     return ws + (slot * Q * C::CONSUMER_WARPS * 32 + (int64_t)warp * 32 + lane) * 4;
 }
 
+// Sum the nseg partial tiles slot_of(0), slot_of(1), ... into acc in that fixed order
+// (deterministic).  Loads are batched -- PB partials x QC 256-bit groups, at most 32 doubles
+// in flight per thread, so the E = 16 instances stay within 128 registers and E = 64 within
+// 255 -- and a batch is issued before any of it is added: about nseg / PB L2 round trips
+// per q-chunk instead of nseg.
+template <class C, int PB_MAX = 32, class SlotOf>
+__device__ __forceinline__ void sum_partials(double (&acc)[C::MB][C::NP][2][2], const double *ws, int nseg,
+                                             SlotOf slot_of, int warp, int lane) {
+    constexpr int Q = C::E / 4;
+    constexpr int64_t QSTRIDE = (int64_t)C::CONSUMER_WARPS * 32 * 4;   // doubles between q groups
+    constexpr int PB0 = C::E >= 32 ? 1 : 32 / C::E;
+    constexpr int PB = PB0 < PB_MAX ? PB0 : PB_MAX;                   // partials in flight
+    constexpr int QC = Q < 8 ? Q : 8;                                  // q groups in flight
+    static_assert(Q % QC == 0, "q chunking");
+    double *flat = &acc[0][0][0][0];
+#pragma unroll
+    for (int e = 0; e < C::E; ++e) flat[e] = 0.0;
+    for (int t0 = 0; t0 < nseg; t0 += PB) {
+#pragma unroll
+        for (int q0 = 0; q0 < Q; q0 += QC) {
+            double v[PB][QC][4];
+#pragma unroll
+            for (int u = 0; u < PB; ++u) {
+                if (t0 + u < nseg) {
+                    const double *src =
+                        partial_slot<C>(const_cast<double *>(ws), slot_of(t0 + u), warp, lane) + q0 * QSTRIDE;
+#pragma unroll
+                    for (int q = 0; q < QC; ++q)
+                        asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];\n"
+                                     : "=d"(v[u][q][0]), "=d"(v[u][q][1]), "=d"(v[u][q][2]), "=d"(v[u][q][3])
+                                     : "l"(src + q * QSTRIDE));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < PB; ++u) {
+                if (t0 + u < nseg) {
+#pragma unroll
+                    for (int q = 0; q < QC; ++q)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) flat[4 * (q0 + q) + e] += v[u][q][e];
+                }
+            }
+        }
+    }
+}
+
 // Deterministic reduction of the nseg partial sums of one tile (split-K slices or
 // stream-K segments).  Partial `seg` goes to workspace slot (tile * stride + seg); the
 // CTA arriving last on the tile's counter adds the nseg partials in segment order (so the
@@ -296,22 +342,7 @@ __device__ __forceinline__ bool partial_reduce(double (&acc)[C::MB][C::NP][2][2]
     __syncthreads();
     if (!s_last) return false;
     __threadfence();
-#pragma unroll
-    for (int e = 0; e < C::E; ++e) flat[e] = 0.0;
-    for (int t = 0; t < nseg; ++t) {
-        const double *src = partial_slot<C>(ws, tile * stride + t, warp, lane);
-#pragma unroll
-        for (int q = 0; q < Q; ++q) {
-            double v0, v1, v2, v3;
-            asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];\n"
-                         : "=d"(v0), "=d"(v1), "=d"(v2), "=d"(v3)
-                         : "l"(src + q * QSTRIDE));
-            flat[4 * q] += v0;
-            flat[4 * q + 1] += v1;
-            flat[4 * q + 2] += v2;
-            flat[4 * q + 3] += v3;
-        }
-    }
+    sum_partials<C>(acc, ws, nseg, [&](int t) { return tile * stride + t; }, warp, lane);
     if (threadIdx.x == 0) counters[tile] = 0;
     return true;
 }
@@ -343,6 +374,7 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
     uint8_t *base_ptr = smem_raw + (base - raw);
     uint64_t *full = reinterpret_cast<uint64_t *>(base_ptr + C::STAGES * C::STAGE_BYTES);
     uint64_t *empty = full + C::STAGES;
+    DG_TRACE_AT(0);
 
     const int tiles_m = (M + C::BM - 1) / C::BM, tiles_n = (N + C::BN - 1) / C::BN;
     int tm, tn;
@@ -370,6 +402,7 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
     }
     if (R > 1 ? lane == 0 : producer) pol = l2_policy_evict_normal();
     griddep_wait();
+    DG_TRACE_AT(1);
     griddep_launch();
     if (producer) {
         for (int s = 0; s < C::STAGES && s < NK; ++s)
@@ -402,6 +435,9 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
             }
             if (R > 1) __syncwarp();   // the refilling lane rejoins before the warp-wide mma.sync
             mbar_wait(&full[s], (i / C::STAGES) & 1);
+#ifdef DG_TRACE
+            if (i == 0) DG_TRACE_AT(2);
+#endif
             const uint32_t sA = base + s * C::STAGE_BYTES;
             mma_stage<C>(sA, sA + C::A_BYTES, fo, acc);
             release_slot(&empty[s], lane);
@@ -447,10 +483,22 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
             }
         }
     }
+    DG_TRACE_AT(3);
+#ifdef DG_TRACE
+    DG_TRACE_SLOT(7, (unsigned long long)dg_smid());
+#endif
     if constexpr (SPLIT) {
-        if (!split_reduce<C>(acc, sk, blockIdx.x, split, warp, lane)) return;
+        if (!split_reduce<C>(acc, sk, blockIdx.x, split, warp, lane)) {
+            DG_TRACE_AT(6);
+            return;
+        }
     }
+    DG_TRACE_AT(4);
     epilogue<C>(acc, m0 + warp_m * C::WM, n0 + warp_n * C::WN, lane, M, N, alpha, beta, Cm, ldc, vec != 0);
+    DG_TRACE_AT(6);
+#ifdef DG_TRACE
+    DG_TRACE_SLOT(7, (unsigned long long)dg_smid() | (1ull << 32));
+#endif
 }
 
 // ------------------------------------------------------------------------------
@@ -484,24 +532,11 @@ __device__ __forceinline__ bool streamk_reduce(double (&acc)[C::MB][C::NP][2][2]
     __syncthreads();
     if (!s_last_sk) return false;
     __threadfence();
-#pragma unroll
-    for (int e = 0; e < C::E; ++e) flat[e] = 0.0;
-    for (int j = 0; j < nseg; ++j) {           // segment order = k order
+    // segment order = k order: segment j of the tile comes from CTA before - 1 + j
+    sum_partials<C, 1>(acc, ws, nseg, [&](int j) {
         const int gj = before - 1 + j;
-        const int slot = 2 * gj + (sk_bound(gj, U, G) >= t0 ? 0 : 1);
-        const double *src = partial_slot<C>(ws, slot, warp, lane);
-#pragma unroll
-        for (int q = 0; q < Q; ++q) {
-            double v0, v1, v2, v3;
-            asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];\n"
-                         : "=d"(v0), "=d"(v1), "=d"(v2), "=d"(v3)
-                         : "l"(src + q * QSTRIDE));
-            flat[4 * q] += v0;
-            flat[4 * q + 1] += v1;
-            flat[4 * q + 2] += v2;
-            flat[4 * q + 3] += v3;
-        }
-    }
+        return (int64_t)(2 * gj + (sk_bound(gj, U, G) >= t0 ? 0 : 1));
+    }, warp, lane);
     if (threadIdx.x == 0) counters[tile] = 0;
     return true;
 }
@@ -517,6 +552,7 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
     uint8_t *base_ptr = smem_raw + (base - raw);
     uint64_t *full = reinterpret_cast<uint64_t *>(base_ptr + C::STAGES * C::STAGE_BYTES);
     uint64_t *empty = full + C::STAGES;
+    DG_TRACE_AT(0);
 
     const int tiles_m = (M + C::BM - 1) / C::BM, tiles_n = (N + C::BN - 1) / C::BN;
     // 32-bit k-step bookkeeping (the host guarantees U = tiles * KT < 2^31) keeps the
@@ -550,6 +586,7 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
         tma_prefetch_desc(&tmB);
     }
     griddep_wait();
+    DG_TRACE_AT(1);
     griddep_launch();
     if (producer) {
         for (int s = 0; s < C::STAGES && s < nloc; ++s) issue_at(s, s);
@@ -581,6 +618,9 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
             }
             __syncwarp();   // the refilling lane rejoins before the warp-wide mma.sync
             mbar_wait(&full[stage], (uint32_t)phase);
+#ifdef DG_TRACE
+            if (li == 0) DG_TRACE_AT(2);
+#endif
             const uint32_t sA = base + stage * C::STAGE_BYTES;
             mma_stage<C>(sA, sA + C::A_BYTES, fo, acc);
             release_slot(&empty[stage], lane);
@@ -596,6 +636,10 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
         int tm, tn;
         tile_coords(tile, tiles_m, tiles_n, group_m, tm, tn);
         bool do_epi = true;
+#ifdef DG_TRACE
+        if (t0 + kb == u0) DG_TRACE_AT(3);                      // first tile of this CTA
+        if (li >= nloc) DG_TRACE_AT(5);                         // last tile
+#endif
         if (nseg > 1) {
             // Partial of CTA g goes to workspace slot 2g (its first unit) or 2g+1 (its last
             // unit); segment j of the tile comes from CTA g_j = before - 1 + j.
@@ -605,9 +649,16 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
         if (do_epi)
             epilogue<C>(acc, tm * C::BM + warp_m * C::WM, tn * C::BN + warp_n * C::WN, lane, M, N, alpha, beta, Cm,
                         ldc, vec != 0);
+#ifdef DG_TRACE
+        if (t0 + kb == u0) DG_TRACE_AT(4);
+#endif
         ++tile;
         kb = 0;
     }
+    DG_TRACE_AT(6);
+#ifdef DG_TRACE
+    DG_TRACE_SLOT(7, (unsigned long long)dg_smid() | ((unsigned long long)(tile - u0 / KT) << 32));
+#endif
 }
 
 // ------------------------------------------------------------------------------

@@ -29,6 +29,11 @@
 
 namespace dg {
 
+#ifdef DG_TRACE
+static void *g_trace_ptr = nullptr;   // gemm_trace_set (instrumented builds)
+void *trace_device_ptr() { return g_trace_ptr; }
+#endif
+
 // C = beta*C (alpha == 0 or K == 0); beta == 0 writes zeros without reading C.
 __global__ void scale_kernel(int M, int N, double beta, double *__restrict__ Cm, int64_t ldc) {
     const int64_t total = (int64_t)M * N;
@@ -399,6 +404,29 @@ static Choice choose_uncached(int64_t M, int64_t N, int64_t K, bool tma, bool si
 
 static int select_cfg(int64_t M, int64_t N, int64_t K, bool tma) { return choose(M, N, K, tma).id; }
 
+// The heuristic restricted to the deterministic split-K configurations with a forced slice
+// count S > 1 (gemm_f64_ex with cfg_id = -1 and splits > 1); -1 if none applies (no TMA).
+static int choose_splitk(int64_t M, int64_t N, int64_t K, bool tma, int S) {
+    if (!tma) return -1;
+    int best = -1;
+    double best_t = 1e300;
+    for (const Cand &c : k_tma_cands) {
+        const int id = find_cfg(c.name);
+        if (id < 0 || g_cfgs[id].d.split_k != 0) continue;
+        int occ = 1;
+        if (prepare_cfg(id, &occ) != GEMM_OK) {
+            clear_error();
+            occ = 1;
+        }
+        const double t = est_time(g_cfgs[id].d, occ, num_sms(), M, N, K, S, c.eff);
+        if (t < best_t * 0.999) {
+            best_t = t;
+            best = id;
+        }
+    }
+    return best;
+}
+
 // splits for a forced split-K configuration (auto): the model's best S for this cfg
 static int auto_splits(int id, int64_t M, int64_t N, int64_t K) {
     int occ = 1;
@@ -423,6 +451,10 @@ static int auto_splits(int id, int64_t M, int64_t N, int64_t K) {
 }
 
 // ---- per-(device, stream) split-K workspace: partials + self-resetting tile counters
+// A buffer that a call has used may be referenced by a CUDA graph captured from that call,
+// so growth never frees it: the old buffer is retired (kept allocated) and a larger one --
+// at least 1.25x, which bounds the retired total by 4x the live size -- takes its place.
+// Retired and live buffers are freed only by gemm_workspace_release().
 struct SplitWs {
     double *ws = nullptr;
     size_t ws_cap = 0;
@@ -433,6 +465,22 @@ struct SplitWs {
 };
 static std::mutex g_ws_mu;
 static std::map<std::pair<int, cudaStream_t>, SplitWs> g_ws;
+static std::vector<std::pair<int, void *>> g_retired;   // (device, buffer), guarded by g_ws_mu
+
+// grow *buf to hold `need` elements of `elem` bytes; the old buffer is retired, not freed
+static bool grow(int dev, void **buf, size_t *cap, size_t need, size_t elem) {
+    if (*cap >= need) return true;
+    const size_t want = std::max(need, *cap + *cap / 4);
+    void *p = nullptr;
+    if (cudaMalloc(&p, want * elem) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    if (*buf) g_retired.push_back({dev, *buf});
+    *buf = p;
+    *cap = want;
+    return true;
+}
 
 // Repack buffer `which` (0 = A, 1 = B) of at least `doubles` elements for stream st.
 static double *get_pack_buf(cudaStream_t st, int which, size_t doubles) {
@@ -440,17 +488,39 @@ static double *get_pack_buf(cudaStream_t st, int which, size_t doubles) {
     if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
     std::lock_guard<std::mutex> lk(g_ws_mu);
     SplitWs &w = g_ws[{dev, st}];
-    if (w.pack_cap[which] < doubles) {
-        if (w.pack[which]) cudaFree(w.pack[which]);
-        w.pack[which] = nullptr;
-        w.pack_cap[which] = 0;
-        if (cudaMalloc(&w.pack[which], doubles * sizeof(double)) != cudaSuccess) {
-            cudaGetLastError();
-            return nullptr;
-        }
-        w.pack_cap[which] = doubles;
-    }
+    if (!grow(dev, (void **)&w.pack[which], &w.pack_cap[which], doubles, sizeof(double))) return nullptr;
     return w.pack[which];
+}
+
+// frees every cached workspace of the current device (after a device synchronize)
+int workspace_release_f64() {
+    int dev = 0;
+    int rc = cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    if (rc) return rc;
+    rc = cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    for (auto it = g_ws.begin(); it != g_ws.end();) {
+        if (it->first.first != dev) {
+            ++it;
+            continue;
+        }
+        SplitWs &w = it->second;
+        cudaFree(w.ws);
+        cudaFree(w.ctr);
+        cudaFree(w.pack[0]);
+        cudaFree(w.pack[1]);
+        it = g_ws.erase(it);
+    }
+    for (auto it = g_retired.begin(); it != g_retired.end();) {
+        if (it->first == dev) {
+            cudaFree(it->second);
+            it = g_retired.erase(it);
+        } else {
+            ++it;
+        }
+    }
+    return GEMM_OK;
 }
 
 static int get_split_ws(cudaStream_t st, size_t doubles, size_t tiles, double **ws, int **ctr);
@@ -475,27 +545,14 @@ static int get_split_ws(cudaStream_t st, size_t doubles, size_t tiles, double **
     if (rc) return rc;
     std::lock_guard<std::mutex> lk(g_ws_mu);
     SplitWs &w = g_ws[{dev, st}];
-    if (w.ws_cap < doubles) {
-        if (w.ws) cudaFree(w.ws);
-        w.ws = nullptr;
-        w.ws_cap = 0;
-        if (cudaMalloc(&w.ws, doubles * sizeof(double)) != cudaSuccess) {
-            cudaGetLastError();
-            return set_error(GEMM_ERR_ALLOC, "split-K workspace of %zu bytes", doubles * sizeof(double));
-        }
-        w.ws_cap = doubles;
-    }
+    if (!grow(dev, (void **)&w.ws, &w.ws_cap, doubles, sizeof(double)))
+        return set_error(GEMM_ERR_ALLOC, "split-K workspace of %zu bytes (cudaMalloc failed%s)", doubles * sizeof(double),
+                         " -- during stream capture, make one eager call of the largest shape first");
     if (w.ctr_cap < tiles) {
-        if (w.ctr) cudaFree(w.ctr);
-        w.ctr = nullptr;
-        w.ctr_cap = 0;
-        if (cudaMalloc(&w.ctr, tiles * sizeof(int)) != cudaSuccess) {
-            cudaGetLastError();
-            return set_error(GEMM_ERR_ALLOC, "split-K counters");
-        }
-        rc = cuda_check(cudaMemsetAsync(w.ctr, 0, tiles * sizeof(int), st), "cudaMemsetAsync(counters)");
+        if (!grow(dev, (void **)&w.ctr, &w.ctr_cap, tiles, sizeof(int)))
+            return set_error(GEMM_ERR_ALLOC, "split-K counters (cudaMalloc failed)");
+        rc = cuda_check(cudaMemsetAsync(w.ctr, 0, w.ctr_cap * sizeof(int), st), "cudaMemsetAsync(counters)");
         if (rc) return rc;
-        w.ctr_cap = tiles;
     }
     *ws = w.ws;
     *ctr = w.ctr;
@@ -610,7 +667,15 @@ int gemm_impl(int64_t M, int64_t N, int64_t K, double alpha, const double *A, in
     }
     int id = cfg_id;
     int splits = 1;
-    if (id < 0) {
+    if (force_splits < 0) return set_error(GEMM_ERR_ARG, "splits=%d must be >= 0", force_splits);
+    if (id < 0 && force_splits > 1) {   // heuristic over the split-K configurations, S forced
+        id = choose_splitk(M, N, K, tma, force_splits);
+        if (id < 0)
+            return set_error(GEMM_ERR_UNSUPPORTED,
+                             "splits=%d needs a *_splitk (TMA) configuration, but A/B miss the TMA rules "
+                             "(16-byte aligned, even lda/ldb)", force_splits);
+        splits = force_splits;
+    } else if (id < 0) {
         const Choice c = choose(M, N, K, tma, force_splits == 1);   // 1: one k-pass per tile
         id = c.id;
         splits = force_splits == 1 ? 1 : c.splits;
@@ -624,7 +689,6 @@ int gemm_impl(int64_t M, int64_t N, int64_t K, double alpha, const double *A, in
     rc = prepare_cfg(id, &occ);
     if (rc) return rc;
     const gemm_cfg_desc &d = g_cfgs[id].d;
-    if (force_splits < 0) return set_error(GEMM_ERR_ARG, "splits=%d must be >= 0", force_splits);
     if (cfg_id >= 0 && d.split_k == 0) splits = force_splits > 0 ? force_splits : auto_splits(id, M, N, K);
     if (d.split_k < 0) splits = 1;   // stream-K / hybrid: the work split is fixed by the grid, not by S
     if (force_splits > 1 && d.split_k != 0)
@@ -762,6 +826,23 @@ int gemm_plan(int64_t M, int64_t N, int64_t K, const double *A, int64_t lda, con
 }
 
 const char *gemm_last_error(void) { return last_error(); }
+
+int gemm_workspace_release(void) {
+    clear_error();
+    const int rc = workspace_release_f64();
+    if (rc) return rc;
+    f32::workspace_release_f32();
+    return GEMM_OK;
+}
+
+#ifdef DG_TRACE
+// instrumented builds only (not declared in include/gemm_f64.h): register a device buffer of
+// 8 u64 per CTA for the per-CTA timeline of the next launches (NULL disables)
+GEMM_API int gemm_trace_set(void *device_buf) {
+    dg::g_trace_ptr = device_buf;
+    return GEMM_OK;
+}
+#endif
 
 const char *gemm_version(void) { return "gemm_f64 0.1 (sm_100a, DMMA.8x8x4, TMA/mbarrier)"; }
 

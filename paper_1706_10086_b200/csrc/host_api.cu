@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <map>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include "../../include/gemm_f64.h"
@@ -199,6 +200,11 @@ static int host_impl(int64_t M, int64_t N, int64_t K, double alpha, const double
         if (!r) r = d2h_block(r0, nr, c0, nc);
         return r;
     };
+    // Everything from here on enqueues asynchronous work that reads A, B, C (host memory the
+    // caller may free once we return): on any error the three streams are drained before the
+    // first error is returned, so the call stays synchronous on its error paths too.
+    auto enqueue = [&]() -> int {
+    int rc = GEMM_OK;
     if ((rc = h2d_a(0, Ra))) return rc;
     for (size_t j = 0; j < cols.size(); ++j) {
         const int64_t c0 = cols[j].first, nc = cols[j].second;
@@ -222,6 +228,16 @@ static int host_impl(int64_t M, int64_t N, int64_t K, double alpha, const double
         const int64_t lcb = last ? std::max<int64_t>(kTn, ((N + nlast - 1) / nlast + kTn - 1) / kTn * kTn) : N;
         for (int64_t c0 = 0; c0 < N; c0 += lcb)
             if ((rc = block(r0, nr, c0, std::min(N, c0 + lcb) - c0))) return rc;
+    }
+    return GEMM_OK;
+    };
+    if ((rc = enqueue())) {
+        const std::string first = last_error();
+        cudaStreamSynchronize(P.h2d);
+        cudaStreamSynchronize(P.comp);
+        cudaStreamSynchronize(P.d2h);
+        cudaGetLastError();
+        return set_error(rc, "%s", first.c_str());
     }
     return cuda_check(cudaStreamSynchronize(P.d2h), "gemm_f64_host synchronize");
 }

@@ -5,7 +5,13 @@
 #include <cuda_runtime.h>
 #include <utility>
 
+#include "ptx.cuh"
+
 namespace dg {
+
+#ifdef DG_TRACE
+void *trace_device_ptr();   // gemm_f64.cu: the buffer gemm_trace_set() registered (or NULL)
+#endif
 
 // Every GEMM kernel is launched with programmatic stream serialization (PDL): it may become
 // resident while the previous kernel of the stream drains and waits for it in-kernel
@@ -32,6 +38,15 @@ static cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, siz
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
+#ifdef DG_TRACE
+    // only when the registered buffer changed, so back-to-back traced launches keep their
+    // programmatic-dependent-launch overlap (no copy node between them)
+    void *tp = trace_device_ptr();
+    if (tp != dg_trace_last) {   // both per translation unit, like dg_trace_buf
+        cudaMemcpyToSymbolAsync(dg_trace_buf, &tp, sizeof(tp), 0, cudaMemcpyHostToDevice, st);
+        dg_trace_last = tp;
+    }
+#endif
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 

@@ -10,6 +10,35 @@
 
 namespace dg {
 
+// ---- optional per-CTA timeline (instrumented builds only: build.py --trace, -DDG_TRACE) ----
+// Each CTA writes 8 u64 at trace[(blockIdx.y * gridDim.x + blockIdx.x) * 8]: globaltimer (ns)
+// at the points the kernels mark with DG_TRACE_AT(slot), and in slot 7 the SM id.  The
+// pointer is per translation unit and set by launch_k before each launch.  Product builds
+// compile all of this away.
+#ifdef DG_TRACE
+static __device__ unsigned long long *dg_trace_buf;
+static void *dg_trace_last = reinterpret_cast<void *>(~uintptr_t(0));   // host copy of dg_trace_buf
+__device__ __forceinline__ unsigned long long dg_gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned dg_smid() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%smid;\n" : "=r"(r));
+    return r;
+}
+#define DG_TRACE_SLOT(slot, val)                                                                     \
+    do {                                                                                             \
+        if (threadIdx.x == 0 && dg_trace_buf)                                                        \
+            dg_trace_buf[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 + (slot)] = (val);         \
+    } while (0)
+#define DG_TRACE_AT(slot) DG_TRACE_SLOT(slot, dg_gtimer())
+#else
+#define DG_TRACE_SLOT(slot, val) ((void)0)
+#define DG_TRACE_AT(slot) ((void)0)
+#endif
+
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

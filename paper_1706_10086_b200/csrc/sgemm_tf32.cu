@@ -27,6 +27,7 @@
 #include <cstdio>
 #include <map>
 #include <mutex>
+#include <vector>
 
 #include "../../include/gemm_f64.h"
 #include "dgemm_kernels.cuh"
@@ -579,22 +580,51 @@ static std::mutex g_mu;
 static std::map<std::pair<int, cudaStream_t>, Ws> g_ws;
 static std::map<int, bool> g_attr;   // (device * 64 + cfg) -> smem attribute set
 
+static std::vector<std::pair<int, float *>> g_retired;   // (device, buffer) kept for captured graphs
+
+// Per-(device, stream) split workspace.  As in gemm_f64.cu: growth retires the old buffer
+// instead of freeing it (a CUDA graph captured from an earlier call may still use it); only
+// gemm_workspace_release() frees.
 static float *workspace(cudaStream_t st, size_t floats) {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
     std::lock_guard<std::mutex> lk(g_mu);
     Ws &w = g_ws[{dev, st}];
     if (w.cap < floats) {
-        if (w.buf) cudaFree(w.buf);
-        w.buf = nullptr;
-        w.cap = 0;
-        if (cudaMalloc(&w.buf, floats * sizeof(float)) != cudaSuccess) {
+        const size_t want = std::max(floats, w.cap + w.cap / 4);
+        float *p = nullptr;
+        if (cudaMalloc(&p, want * sizeof(float)) != cudaSuccess) {
             cudaGetLastError();
             return nullptr;
         }
-        w.cap = floats;
+        if (w.buf) g_retired.push_back({dev, w.buf});
+        w.buf = p;
+        w.cap = want;
     }
     return w.buf;
+}
+
+// frees the current device's FP32 workspace (the caller has synchronized the device)
+void workspace_release_f32() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (auto it = g_ws.begin(); it != g_ws.end();) {
+        if (it->first.first == dev) {
+            cudaFree(it->second.buf);
+            it = g_ws.erase(it);
+        } else {
+            ++it;
+        }
+    }
+    for (auto it = g_retired.begin(); it != g_retired.end();) {
+        if (it->first == dev) {
+            cudaFree(it->second);
+            it = g_retired.erase(it);
+        } else {
+            ++it;
+        }
+    }
 }
 
 static bool overlaps(const void *p, int64_t rows, int64_t cols, int64_t ld, const void *q, int64_t qrows,

@@ -31,6 +31,8 @@ struct Comm {
     std::vector<cudaEvent_t> ev;
     double *ws = nullptr;
     size_t ws_cap = 0;
+    cudaEvent_t ws_free = nullptr;   // recorded after the last reader of ws (previous call)
+    bool ws_free_valid = false;
 };
 
 static int nccl_check(ncclResult_t r, const char *what) {
@@ -99,6 +101,7 @@ int gemm_comm_destroy(void *comm) {
     int rc = GEMM_OK;
     if (c->nccl) rc = nccl_check(ncclCommDestroy(c->nccl), "ncclCommDestroy");
     for (auto e : c->ev) cudaEventDestroy(e);
+    if (c->ws_free) cudaEventDestroy(c->ws_free);
     if (c->ws) cudaFree(c->ws);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     delete c;
@@ -144,7 +147,13 @@ int gemm_f64_sharded(int64_t M_local, int64_t N, int64_t K, double alpha, const 
     }
 
     // ---- column-panel pipeline ----
+    if (!c->ws_free &&
+        (rc = cuda_check(cudaEventCreateWithFlags(&c->ws_free, cudaEventDisableTiming), "cudaEventCreate")))
+        return rc;
     if (c->ws_cap < (size_t)(K * N)) {
+        // the previous call's GEMMs (on whatever stream it used) may still read the old panels
+        if (c->ws_free_valid && (rc = cuda_check(cudaEventSynchronize(c->ws_free), "cudaEventSynchronize")))
+            return rc;
         if (c->ws) cudaFree(c->ws);
         c->ws = nullptr;
         c->ws_cap = 0;
@@ -160,8 +169,11 @@ int gemm_f64_sharded(int64_t M_local, int64_t N, int64_t K, double alpha, const 
     nch = (int)((N + w - 1) / w);
     const bool is_root = (c->rank == root);
     // comm stream starts after prior work on the caller's stream (B / C may be written there)
+    // and after the previous call's last GEMM, which read the panels it is about to overwrite
     if ((rc = cuda_check(cudaEventRecord(c->ev[nch], st), "event"))) return rc;
     if ((rc = cuda_check(cudaStreamWaitEvent(c->comm_stream, c->ev[nch], 0), "wait"))) return rc;
+    if (c->ws_free_valid && (rc = cuda_check(cudaStreamWaitEvent(c->comm_stream, c->ws_free, 0), "wait")))
+        return rc;
     for (int j = 0; j < nch; ++j) {
         const int64_t n0 = j * w, nw = std::min(N, n0 + w) - n0;
         double *panel = c->ws + K * n0;   // packed K x nw
@@ -188,7 +200,11 @@ int gemm_f64_sharded(int64_t M_local, int64_t N, int64_t K, double alpha, const 
         }
     }
     if ((rc = cuda_check(cudaEventRecord(c->ev[nch + 1], c->comm_stream), "event"))) return rc;
-    return cuda_check(cudaStreamWaitEvent(st, c->ev[nch + 1], 0), "wait");
+    if ((rc = cuda_check(cudaStreamWaitEvent(st, c->ev[nch + 1], 0), "wait"))) return rc;
+    // every reader of the panels (this call's GEMMs and the unpack) is ordered before this point
+    if ((rc = cuda_check(cudaEventRecord(c->ws_free, st), "event"))) return rc;
+    c->ws_free_valid = true;
+    return GEMM_OK;
 }
 
 }  // extern "C"

@@ -12,7 +12,9 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgemm_f64.so")
+# GEMM_F64_LIB: load another build of the same library instead (the instrumented
+# libgemm_f64_trace.so of tools/trace_ctas.py); unset in every product / test / bench run
+LIB_PATH = os.environ.get("GEMM_F64_LIB") or os.path.join(_HERE, "libgemm_f64.so")
 
 GEMM_OK, GEMM_ERR_ARG, GEMM_ERR_CUDA, GEMM_ERR_NCCL, GEMM_ERR_UNSUPPORTED, GEMM_ERR_ALLOC = range(6)
 STATUS_NAMES = {0: "GEMM_OK", 1: "GEMM_ERR_ARG", 2: "GEMM_ERR_CUDA", 3: "GEMM_ERR_NCCL",
@@ -22,6 +24,7 @@ FILL_MODES = {"uniform": 0, "dyadic": 1, "int8": 2, "ones": 3, "identity": 4, "z
 # every symbol include/gemm_f64.h declares (tests check the library exports them all)
 EXPORTS = ("gemm_f64", "gemm_f64_stream", "gemm_f64_cfg", "gemm_f64_ex", "gemm_f32", "gemm_f32_stream",
            "gemm_f32_cfg", "gemm_f32_num_cfgs", "gemm_f32_cfg_name", "gemm_f64_host", "gemm_host_pool_release",
+           "gemm_workspace_release",
            "gemm_num_cfgs", "gemm_cfg_name", "gemm_cfg_info", "gemm_cfg_select", "gemm_plan", "gemm_plan_set",
            "gemm_plan_clear", "gemm_tune_load", "gemm_last_error",
            "gemm_fill_f64", "gemm_peak_probe", "gemm_comm_unique_id", "gemm_comm_init",
@@ -58,6 +61,7 @@ def _load():
         "gemm_f32_cfg_name": (ci, [ci, ctypes.c_char_p, ci]),
         "gemm_f64_host": (ci, core),
         "gemm_host_pool_release": (ci, []),
+        "gemm_workspace_release": (ci, []),
         "gemm_num_cfgs": (ci, []),
         "gemm_cfg_name": (ci, [ci, ctypes.c_char_p, ci]),
         "gemm_cfg_info": (ci, [ci, ctypes.POINTER(CfgDesc)]),
@@ -125,7 +129,9 @@ def _dtype(name):
 
 
 def _mat(x, name, dtype="float64"):
-    """(ptr, rows, cols, ld) of a 2-D float64 (or float32) tensor with unit column stride.
+    """(ptr, rows, cols, ld) of a 2-D float64 (or float32) tensor with unit column stride and
+    non-overlapping rows (row stride >= cols; a zero-stride expand() or a negative stride is
+    rejected, since the kernel would address rows*ld elements of a smaller buffer).
     Per-call cost matters for small GEMMs: one attribute access each (no string work)."""
     if x.dtype is not _dtype(dtype):
         raise TypeError(f"{name} must be {dtype}, got {x.dtype}")
@@ -138,9 +144,11 @@ def _mat(x, name, dtype="float64"):
     s0, s1 = x.stride()
     if c > 1 and s1 != 1:
         raise ValueError(f"{name} must have unit stride along columns (row-major)")
-    ld = s0 if (r > 1 or s0 >= c) else c
-    ld = max(ld, c, 1)
-    return x.data_ptr(), r, c, ld
+    if r > 1:
+        if s0 < c or s0 <= 0:
+            raise ValueError(f"{name} has overlapping rows (row stride {s0} < {c} columns): make it contiguous")
+        return x.data_ptr(), r, c, s0
+    return x.data_ptr(), r, c, c   # a single row never uses its leading dimension
 
 
 _RAW_STREAM = None
@@ -168,6 +176,19 @@ def _stream_ptr(stream):
     return stream.cuda_stream
 
 
+def _on_current_device(*ts, names="ABC"):
+    """Every tensor is a CUDA tensor on the current device (the library launches there)."""
+    import torch
+    dev = torch.cuda.current_device()
+    for t, n in zip(ts, names):
+        d = t.get_device()   # -1 for CPU tensors
+        if d != dev:
+            if d < 0:
+                raise ValueError(f"{n} must be a CUDA tensor (use gemm_host for host buffers)")
+            raise ValueError(f"{n} is on cuda:{d} but the current device is cuda:{dev} "
+                             "(torch.cuda.set_device or move the tensor)")
+
+
 def gemm(A, B, C, alpha: float = 1.0, beta: float = 0.0, cfg: int | None = None, stream=None,
          splits: int | None = None):
     """C <- alpha*A@B + beta*C on the GPU (torch CUDA float64 tensors, row-major). Returns C."""
@@ -176,9 +197,7 @@ def gemm(A, B, C, alpha: float = 1.0, beta: float = 0.0, cfg: int | None = None,
     pc, M2, N2, ldc = _mat(C, "C")
     if K2 != K or M2 != M or N2 != N:
         raise ValueError(f"shape mismatch A{tuple(A.shape)} B{tuple(B.shape)} C{tuple(C.shape)}")
-    for t, n in ((A, "A"), (B, "B"), (C, "C")):
-        if not t.is_cuda:
-            raise ValueError(f"{n} must be a CUDA tensor (use gemm_host for host buffers)")
+    _on_current_device(A, B, C)
     st = _stream_ptr(stream)
     if cfg is None and splits is None:
         rc = _lib.gemm_f64_stream(M, N, K, float(alpha), pa, lda, pb, ldb, float(beta), pc, ldc, st)
@@ -199,6 +218,7 @@ def gemm_f32(A, B, C, alpha: float = 1.0, beta: float = 0.0, stream=None, cfg: i
     pc, M2, N2, ldc = _mat(C, "C", "float32")
     if K2 != K or M2 != M or N2 != N:
         raise ValueError(f"shape mismatch A{tuple(A.shape)} B{tuple(B.shape)} C{tuple(C.shape)}")
+    _on_current_device(A, B, C)
     if cfg is None:
         _check(_lib.gemm_f32_stream(M, N, K, float(alpha), pa, lda, pb, ldb, float(beta), pc, ldc,
                                     _stream_ptr(stream)))
@@ -227,13 +247,20 @@ def gemm_host(A, B, C, alpha: float = 1.0, beta: float = 0.0):
     """C <- alpha*A@B + beta*C with HOST buffers (numpy arrays or CPU torch tensors)."""
     def info(x, name):
         if hasattr(x, "data_ptr"):
+            if x.get_device() >= 0:
+                raise ValueError(f"{name} must be a host (CPU) tensor for gemm_host")
             return _mat(x, name)
         import numpy as np
         if x.dtype != np.float64 or x.ndim != 2 or (x.shape[1] > 1 and x.strides[1] != 8):
             raise ValueError(f"{name} must be a row-major float64 2-D array")
         r, c = x.shape
-        ld = max(x.strides[0] // 8 if r > 1 else c, c, 1)
-        return x.ctypes.data, r, c, ld
+        if r > 1 and x.shape[1] > 0:
+            s0 = x.strides[0]
+            if s0 <= 0 or s0 % 8 or s0 // 8 < c:
+                raise ValueError(f"{name} row stride {s0} bytes is negative, not a multiple of 8 or "
+                                 f"overlapping (< {c} doubles): make it contiguous")
+            return x.ctypes.data, r, c, s0 // 8
+        return x.ctypes.data, r, c, max(c, 1)
     pa, M, K, lda = info(A, "A")
     pb, K2, N, ldb = info(B, "B")
     pc, M2, N2, ldc = info(C, "C")
@@ -245,6 +272,12 @@ def gemm_host(A, B, C, alpha: float = 1.0, beta: float = 0.0):
 
 def host_pool_release():
     _check(_lib.gemm_host_pool_release())
+
+
+def workspace_release():
+    """Free the library's cached device workspace on the current device (gemm_workspace_release);
+    CUDA graphs captured from earlier calls must not be replayed afterwards."""
+    _check(_lib.gemm_workspace_release())
 
 
 # ------------------------------------------------------------------ configs
@@ -338,6 +371,7 @@ def fill(X, mode: str, seed: int, mat: int, rows: int | None = None, row0: int =
     """Fill device tensor X (nrows x cols) with rows [row0, row0+nrows) of the logical
     rows x cols matrix of synth's counter-based generator (bitwise identical)."""
     px, nrows, cols, ldx = _mat(X, "X")
+    _on_current_device(X, names=("X",))
     if rows is None:
         rows = row0 + nrows
     _check(_lib.gemm_fill_f64(FILL_MODES[mode], int(seed) & (2 ** 64 - 1), int(mat), int(rows), int(cols),
@@ -375,6 +409,7 @@ class Comm:
         pc, M2, N2, ldc = _mat(C_local, "C_local")
         if K2 != K or M2 != M or N2 != N:
             raise ValueError("shape mismatch")
+        _on_current_device(A_local, B, C_local, names=("A_local", "B", "C_local"))
         _check(_lib.gemm_f64_sharded(M, N, K, float(alpha), pa, lda, pb, ldb, float(beta), pc, ldc,
                                      self._h, int(root), int(bcast_chunks), _stream_ptr(stream)))
         return C_local

@@ -214,3 +214,32 @@ def test_hybrid_launch_count(G):
     assert G.launches_per_call(hyb, 300, 200, 2000) == 2          # no full wave: tail + fix-up
     info = G.cfg_info(hyb)
     assert info["split_k"] == -2 and info["tma"] == 1
+
+
+def test_binding_rejects_overlapping_and_negative_row_strides(G):
+    """a zero-stride expand() (rows alias one buffer row) or a numpy row stride that
+    is negative / not a multiple of 8 / overlapping must raise before any library call --
+    the kernel would otherwise address rows*ld elements of a smaller buffer."""
+    import numpy as np
+    import torch
+    ok = torch.zeros((3, 4), dtype=torch.float64)
+    assert G._mat(ok, "A") == (ok.data_ptr(), 3, 4, 4)
+    assert G._mat(torch.zeros((5, 8), dtype=torch.float64)[:, :3], "A")[3] == 8   # padded ld
+    assert G._mat(torch.zeros((1, 8), dtype=torch.float64).expand(1, 8), "A")[3] == 8   # one row: ld unused
+    with pytest.raises(ValueError, match="overlapping"):
+        G._mat(torch.zeros((1, 8), dtype=torch.float64).expand(6, 8), "A")
+    good = np.zeros((4, 4))
+    for bad in (np.broadcast_to(np.zeros((1, 4)), (4, 4)), good[::-1], np.zeros((4, 9))[:, ::2]):
+        with pytest.raises(ValueError):
+            G.gemm_host(bad, good, np.zeros((4, 4)))
+    with pytest.raises(ValueError, match="stride"):
+        G.gemm_host(np.zeros((4, 4)), good, np.zeros((4, 4))[::-1])
+
+
+def test_forced_splits_without_tma_is_rejected_explicitly(G):
+    """gemm_f64_ex(cfg_id = -1, splits > 1) restricts the heuristic to split-K configurations;
+    with operands that miss the TMA rules (odd lda) there is none: GEMM_ERR_UNSUPPORTED with a
+    message, instead of silently running something else."""
+    lib = G.lib()
+    rc = lib.gemm_f64_ex(8, 8, 7, 1.0, 16, 7, 1024, 8, 0.0, 4096, 8, -1, 4, None)
+    assert rc == G.GEMM_ERR_UNSUPPORTED and "splits=4" in G.last_error(), G.last_error()
