@@ -1,7 +1,8 @@
 """Benchmark of the one hot path: FP64 GEMM C = alpha*A*B + beta*C on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload square|rect|large]
-                    [--impl ours|reference] [--no-e2e] [--no-cpu-baseline]
+    python bench.py [--gpus N] [--steps K] [--warmup W]
+                    [--workload square|rect|large|large_strong] [--bcast-chunks C]
+                    [--impl ours|reference] [--no-e2e] [--no-cpu-baseline] [--verify-rows R]
 
 Multi-GPU: torchrun --nproc-per-node N bench.py --gpus N ...  (one process per GPU).
 
@@ -12,12 +13,21 @@ Workloads (BASELINE.json configs):
           NVLink with NCCL every step (row-block sharding).
   rect:   config 4, M=32768, N=K=4096 row-sharded over the ranks (strong scaling).
   large:  config 5, N=65536 square; 8192 rows per rank (weak).
+  large_strong: config 5 strong: M=N=K=65536 split over the ranks (1 GPU: 96 GiB of
+          operands, the T1 of E_s(P) = T1 / (P T_P)).
 
-A step = broadcast of B (N>1) + one DGEMM launch over the rank's rows.  Inputs are
-device-resident and larger than L2 (>= 128 MiB each at the default workload), so no
-L2 flush is needed.  Time = CUDA events on the launching stream over exactly K
-steps after W warm-ups, barrier + synchronize on both sides, max over ranks.
-value = 2*M*N*K*K_steps / time (Eq. (4) P:93-97 convention, 2MNK).
+A step = one collective call of the sharded entry point gemm_f64_sharded (broadcast of B
+from rank 0, then the local DGEMM over the rank's rows) at N > 1 or under torchrun, and
+one gemm_f64 launch at N = 1.  Inputs are device-resident and larger than L2 (>= 128 MiB
+each at the default workload), so no L2 flush is needed.  Time = CUDA events on the
+launching stream over exactly K steps after W warm-ups, barrier + synchronize on both
+sides, max over ranks.  value = 2*M*N*K*K_steps / time (Eq. (4) P:93-97 convention, 2MNK).
+
+After the timed region every rank checks its own result (post-timing, test
+infrastructure, never inside the timed region): B's bytes against the device generator
+(the broadcast delivered B intact) and R sampled rows of its C shard -- the first, the
+last and random ones, over a block of up to 2048 columns -- against the CPU oracle within
+the north-star bound.  The line carries "parity" (max over ranks); a mismatch exits 1.
 """
 
 from __future__ import annotations
@@ -37,6 +47,8 @@ sys.path.insert(0, ROOT)
 METRIC = "DGEMM TFLOP/s and % of B200 FP64 peak at N=16384 (1 GPU) and 1/2/4/8 GPUs"
 FP64_DATASHEET_TFLOPS = 37.0      # HGX B200: 296 TFLOP/s FP64 / FP64 tensor per 8 GPUs
 BF16_NOMINAL_TFLOPS = 2250.0      # B200_PROFILING.md nominal dense bf16
+# the oracle timed on the GPU box's host: 1 thread / all threads, full runs N=256..4096 (tools/cpu_table.py)
+CPU_TABLE = "profiles/r02/cpu_baseline_table.json"
 
 
 def parse():
@@ -44,7 +56,10 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="square", choices=["square", "rect", "large"])
+    ap.add_argument("--workload", default="square", choices=["square", "rect", "large", "large_strong"])
+    ap.add_argument("--bcast-chunks", type=int, default=1,
+                    help="gemm_f64_sharded column panels (1: broadcast of B, then the GEMM)")
+    ap.add_argument("--verify-rows", type=int, default=4, help="sampled rows per rank checked against the oracle")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
@@ -73,7 +88,7 @@ def stdout_to_stderr(fn):
 
 
 def workload(name, world):
-    """(M_total, N, K, rows_per_rank list, scaling, description)."""
+    """(M_total, N, K, scaling, description)."""
     if name == "square":
         n = 16384
         M = n * world
@@ -81,7 +96,19 @@ def workload(name, world):
     if name == "rect":
         return 32768, 4096, 4096, "strong", "dgemm_m32768_n4096_k4096_rowsharded"
     n = 65536
+    if name == "large_strong":
+        return n, n, n, "strong", f"dgemm_n{n}_rowsharded"
     return 8192 * world, n, n, "weak", f"dgemm_n{n}_rows8192_per_gpu"
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 # ---------------------------------------------------------------------- clocks
@@ -164,7 +191,8 @@ def cpu_oracle_sample(M, N, K, seconds, seed=1706):
         oracle.dgemm(1.0, A, B, 0.0, C, nthreads=threads)
         dt = time.perf_counter() - t0
     return {"value": 2.0 * R * N * K / dt / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
-            "sample": f"{R} rows of the {M}x{N}x{K} problem (i-k-j C oracle, -O2, {threads} threads), {dt:.2f} s"}
+            "sample": f"{R} rows of the {M}x{N}x{K} problem (i-k-j C oracle, -O2, {threads} threads), {dt:.2f} s",
+            "cpu_model": cpu_model(), "table": CPU_TABLE}
 
 
 def run_reference(a):
@@ -198,10 +226,100 @@ def run_reference(a):
             "config": {"workload": wname, "M": M, "N": N, "K": K, "alpha": 1.0, "beta": 0.0,
                        "sample_rows_per_step": R, "parallelism": "host threads"},
             "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
-                             "sample": f"{R} rows of the {M}x{N}x{K} problem per step (i-k-j C oracle)"},
+                             "sample": f"{R} rows of the {M}x{N}x{K} problem per step (i-k-j C oracle)",
+                             "cpu_model": cpu_model(), "table": CPU_TABLE},
             "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+# ---------------------------------------------------------------------- parity (post-timing)
+def sample_rows(Ml, nrows, seed):
+    """Local row indices checked on a rank: first, last and random ones (sorted, unique)."""
+    import numpy as np
+    if Ml <= 0:
+        return []
+    rng = np.random.default_rng(seed)
+    extra = rng.integers(0, Ml, max(0, nrows - 2)).tolist()
+    return sorted({0, Ml - 1, *extra})
+
+
+def check_rows(got, M, N, K, r0, rows, seed, col0, ncols):
+    """Oracle check of C[r0 + rows, col0:col0+ncols] of the bench problem (alpha=1, beta=0,
+    uniform inputs of `seed`): regenerates A's rows and B's column block on the host (synth)
+    and compares `got` (len(rows) x ncols) within the north-star bound.  Returns
+    (ok, max_err_over_bound)."""
+    import numpy as np
+
+    import oracle
+    import synth
+    if not rows or ncols == 0:
+        return True, 0.0
+    A = np.vstack([synth.matrix("uniform", seed, synth.MAT_A, M, K, row0=r0 + i, nrows=1) for i in rows])
+    B = synth.matrix("uniform", seed, synth.MAT_B, K, N, col0=col0, ncols=ncols)
+    ref, mag = oracle.dgemm(1.0, A, B, 0.0, np.zeros((len(rows), ncols)), want_mag=True)
+    r = oracle.check(np.asarray(got, dtype=np.float64), ref, oracle.bound(K, 1.0, 0.0, mag, None))
+    return bool(r.ok), float(r.max_ratio)
+
+
+def reduce_parity(ok, ratio, b_ok, nrows, world, device=None):
+    """Combine per-rank results: ok = all ranks ok, max_ratio = max over ranks."""
+    bad = 0.0 if (ok and b_ok) else 1.0
+    if world > 1:
+        bad, ratio, bbad, nrows = max_over_ranks_sum(bad, ratio, 0.0 if b_ok else 1.0, nrows, world, device)
+        b_ok = bbad == 0.0
+    return {"ok": bad == 0.0, "max_ratio": ratio, "b_bitwise": bool(b_ok), "rows_checked_total": int(nrows)}
+
+
+def max_over_ranks_sum(bad, ratio, bbad, nrows, world, device):
+    """(max, max, max, sum) over ranks (torch.distributed, any backend)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([bad, ratio, bbad], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    n = torch.tensor([float(nrows)], dtype=torch.float64, device=device)
+    dist.all_reduce(n, op=dist.ReduceOp.SUM)
+    return float(t[0]), float(t[1]), float(t[2]), float(n[0])
+
+
+def verify(G, dB, dC, M, N, K, r0, Ml, rank, nrows, seed=1706):
+    """Post-timing self-check of one rank: B's bytes vs the device generator, sampled rows of
+    the local C vs the oracle.  Returns (ok, max_ratio, b_ok, rows_checked, detail)."""
+    import torch
+    b_ok = True
+    slab = max(1, min(K, (1 << 27) // max(N, 1)))          # <= 1 GiB of regenerated B at a time
+    tmp = torch.empty((slab, N), dtype=torch.float64, device=dB.device)
+    for k0 in range(0, K, slab):
+        nk = min(slab, K - k0)
+        G.fill(tmp[:nk], "uniform", seed, 1, rows=K, row0=k0)
+        b_ok = b_ok and bool(torch.equal(tmp[:nk], dB[k0:k0 + nk]))
+    del tmp
+    rows = sample_rows(Ml, nrows, seed + 7919 * rank)
+    ncols = min(N, 2048)
+    col0 = 0 if N == ncols else int((seed + 131 * rank) % ((N - ncols) // 16 + 1)) * 16
+    got = torch.stack([dC[i, col0:col0 + ncols] for i in rows]).cpu().numpy() if rows else None
+    ok, ratio = check_rows(got, M, N, K, r0, rows, seed, col0, ncols)
+    return ok, ratio, b_ok, len(rows), {"rows_local": rows, "col0": col0, "ncols": ncols}
+
+
+def measure_fp64_roof(G, reps=3):
+    """The FP64 tensor-pipe roof measured in-run: gemm_peak_probe, DMMA.8x8x4, 148 blocks x 16
+    warps x 8 independent accumulator chains (Eq. (8) P:259-262, P = f*o*n measured);
+    best of `reps` ~50 ms bursts.  TFLOP/s."""
+    import torch
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    blocks, warps, iters = sms, 16, 100000
+    out = torch.zeros(blocks, dtype=torch.float64, device="cuda")
+    G.peak_probe("dmma", blocks, warps, 2000, out)
+    best = 0.0
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        G.peak_probe("dmma", blocks, warps, iters, out)
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, blocks * warps * iters * 8 * 512 / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+    return best
 
 
 def run_e2e(a, G, dist, comm, stream, dA, dB, dC, M, N, K, Ml, world, flops_step):
@@ -263,8 +381,8 @@ def main():
         print(f"warning: --gpus {a.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
     torch.cuda.set_device(local)
     # launched by torchrun (even with one rank): take the distributed path -- process group,
-    # library NCCL communicator, broadcast of B every step -- so N=1 under torchrun runs
-    # the same code as N>1 (an in-place 1-rank broadcast is a no-op)
+    # library NCCL communicator, gemm_f64_sharded every step -- so N=1 under torchrun runs
+    # the same code as N>1 (a 1-rank broadcast is a no-op)
     distributed = world > 1 or "TORCHELASTIC_RUN_ID" in os.environ or "GEMM_BENCH_FORCE_DIST" in os.environ
     if distributed:
         stdout_to_stderr(lambda: dist.init_process_group("nccl", device_id=torch.device("cuda", local)))
@@ -282,16 +400,22 @@ def main():
         dB.zero_()
     G.fill(dC, "uniform", 1706, 2, rows=M, row0=r0)
     stream = torch.cuda.current_stream()
-    # B's broadcast goes through the library's own NCCL communicator (gemm_comm_init).  If that
-    # cannot be created on some rank, every rank falls back to the same NCCL broadcast through
-    # torch's process group, so the scaling run still measures the sharded path; the line says so.
-    comm, bcast_via = None, None
+    # The step at N > 1 is the library's sharded entry point (gemm_f64_sharded: broadcast of B
+    # over its own NCCL communicator, then the local GEMM).  If that communicator cannot be
+    # created on some rank, every rank falls back to torch's NCCL broadcast + gemm_f64, so the
+    # scaling run still measures the sharded path; the line says so.
+    comm, step_via = None, "gemm_f64 (1 GPU)"
     if distributed:
         err = None
         try:
             if os.environ.get("GEMM_BENCH_TORCH_BCAST"):   # exercise the fallback (tests)
                 raise RuntimeError("forced by GEMM_BENCH_TORCH_BCAST")
             comm = stdout_to_stderr(lambda: G.Comm(rank, world))
+            n_nccl, r_nccl = comm.info()
+            print(f"[rank {rank}] library NCCL communicator: ncclCommCount={n_nccl} ncclCommUserRank={r_nccl} "
+                  f"rows [{r0}, {r1})", file=sys.stderr, flush=True)
+            if n_nccl != world or r_nccl != rank:
+                raise RuntimeError(f"NCCL reports {n_nccl} ranks / rank {r_nccl}, expected {world} / {rank}")
         except Exception as ex:  # noqa: BLE001 -- reported in the JSON line
             err = f"{type(ex).__name__}: {ex}"[:200]
         ok = torch.tensor([0.0 if err else 1.0], device="cuda")
@@ -300,28 +424,44 @@ def main():
             if comm is not None:
                 comm.close()
             comm = None
-            bcast_via = "torch.distributed NCCL broadcast (library communicator failed: " + (err or "on another rank") + ")"
+            step_via = "torch.distributed NCCL broadcast + gemm_f64 (library communicator failed: " + \
+                (err or "on another rank") + ")"
         else:
-            bcast_via = "libgemm_f64 NCCL communicator (gemm_bcast_f64)"
-    # the product's own plan (heuristic entry point) unless a configuration is forced
+            step_via = f"gemm_f64_sharded (library NCCL communicator, bcast_chunks={a.bcast_chunks})"
+    # the product's own plan (heuristic entry point) unless a configuration is forced; the
+    # sharded entry point runs the one-k-pass plan of each column panel (bitwise equal to 1 GPU)
     cfg = a.cfg if a.cfg >= 0 else None
-    plan_cfg, plan_splits = G.plan(Ml, N, K, dA.data_ptr(), K, dB.data_ptr(), N)
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    if comm is not None:
+        if cfg is not None:
+            print("warning: --cfg is ignored by gemm_f64_sharded (it runs the product plan)", file=sys.stderr)
+            cfg = None
+        panels = G.sharded_panels(N, a.bcast_chunks)
+        plans = [G.plan(Ml, w, K, dA.data_ptr(), K, dB.data_ptr(), w if len(panels) > 1 else N, one_pass=True)
+                 for _, w in panels]
+        plan_cfg, plan_splits = plans[-1 if len(panels) == 1 else 0]
+        launches_per_step = sum(G.launches_per_call(c, Ml, w, K, sms) for (c, _), (_, w) in zip(plans, panels))
+    else:
+        plan_cfg, plan_splits = G.plan(Ml, N, K, dA.data_ptr(), K, dB.data_ptr(), N)
+        launches_per_step = G.launches_per_call(cfg if cfg is not None else plan_cfg, Ml, N, K, sms)
     cfg_name = G.cfg_name(cfg if cfg is not None else plan_cfg)
     if cfg is None and plan_splits > 1:
         cfg_name += f" (split-K x{plan_splits})"
-    sms = torch.cuda.get_device_properties(local).multi_processor_count
-    launches_per_step = G.launches_per_call(cfg if cfg is not None else plan_cfg, Ml, N, K, sms)
 
     def step(evs=None):
-        if comm is not None:
-            comm.bcast(dB, root=0, stream=stream)
-        elif distributed:
-            dist.broadcast(dB, src=0)
         if evs is not None:
             evs[0].record(stream)
-        G.gemm(dA, dB, dC, 1.0, 0.0, cfg=cfg, stream=stream)
+        if comm is not None:
+            comm.gemm_sharded(dA, dB, dC, 1.0, 0.0, root=0, bcast_chunks=a.bcast_chunks, stream=stream)
+        else:
+            if distributed:
+                dist.broadcast(dB, src=0)
+            G.gemm(dA, dB, dC, 1.0, 0.0, cfg=cfg, stream=stream)
         if evs is not None:
             evs[1].record(stream)
+
+    # the FP64 roof of this GPU, measured in this run before the timed region (DMMA probe)
+    peak_measured = measure_fp64_roof(G)
 
     for _ in range(a.warmup):
         step()
@@ -340,11 +480,11 @@ def main():
     sampler = ClockSampler(smi_index)
     sampler.start()
     time.sleep(0.3)
-    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
     e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e_start.record(stream)
     for i in range(a.steps):
-        step(kev[i])
+        step(sev[i])
     e_end.record(stream)
     torch.cuda.synchronize()
     if distributed:
@@ -352,21 +492,52 @@ def main():
     torch.cuda.synchronize()
     sampler.stop()
     t_ms = e_start.elapsed_time(e_end)
-    k_ms = [s.elapsed_time(e) for s, e in kev]
-    k_mean = statistics.mean(k_ms)
-    t_ms, k_mean = G.max_over_ranks([t_ms, k_mean], world, device="cuda")
+    s_ms = [s.elapsed_time(e) for s, e in sev]
+    clocks = sampler.summary()
+
+    # ---- the dominant kernel alone (roofline) and the exchange alone, after the timed region:
+    # at N = 1 the step IS the kernel; at N > 1 the GEMM and the broadcast are timed apart
+    if distributed:
+        kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(3)]
+        for s_, e_ in kev:   # the sharded call's GEMM: one-k-pass plan over all N columns
+            s_.record(stream)
+            G.gemm(dA, dB, dC, 1.0, 0.0, stream=stream, splits=1 if comm is not None else None)
+            e_.record(stream)
+        bev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(3)]
+        for s_, e_ in bev:
+            s_.record(stream)
+            if comm is not None:
+                comm.bcast(dB, root=0, stream=stream)
+            else:
+                dist.broadcast(dB, src=0)
+            e_.record(stream)
+        torch.cuda.synchronize()
+        k_mean = statistics.mean(s_.elapsed_time(e_) for s_, e_ in kev)
+        b_mean = statistics.mean(s_.elapsed_time(e_) for s_, e_ in bev)
+    else:
+        k_mean, b_mean = statistics.mean(s_ms), 0.0
+    t_ms, k_mean, b_mean = G.max_over_ranks([t_ms, k_mean, b_mean], world, device="cuda")
     flops_step = 2.0 * M * N * K
     value = flops_step * a.steps / (t_ms * 1e-3) / 1e12
     flops_local = 2.0 * Ml * N * K
     achieved = flops_local / (k_mean * 1e-3) / 1e12
-    clocks = sampler.summary()
+
+    # ---- every rank checks its own result (post-timing)
+    v_ok, v_ratio, v_b, v_rows, v_detail, v_err = False, float("inf"), False, 0, {}, None
+    try:
+        v_ok, v_ratio, v_b, v_rows, v_detail = verify(G, dB, dC, M, N, K, r0, Ml, rank, a.verify_rows)
+    except Exception as ex:  # noqa: BLE001 -- a failed check is a parity failure, reported
+        v_err = f"{type(ex).__name__}: {ex}"[:300]
+    print(f"[rank {rank}] parity: rows {v_detail.get('rows_local')} (+{r0}) cols "
+          f"[{v_detail.get('col0')}, +{v_detail.get('ncols')}) ok={v_ok} max err/bound={v_ratio:.3e} "
+          f"B bitwise={v_b} {v_err or ''}", file=sys.stderr, flush=True)
+    parity = reduce_parity(v_ok, v_ratio, v_b, v_rows, world if distributed else 1, device="cuda")
+    parity["check"] = ("per rank: B vs the device generator (bitwise); first, last and random rows of the "
+                       "local C over <= 2048 columns vs the CPU oracle (north-star bound); max over ranks")
+    if v_err:
+        parity["error_rank0" if rank == 0 else "error"] = v_err
 
     # ---- roofline of the dominant (only) kernel ------------------------------------
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except (OSError, ValueError):
-        pass
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
@@ -376,27 +547,34 @@ def main():
             traffic = ent["dram_bytes_per_launch"]
     except (OSError, ValueError, KeyError):
         pass
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_DATASHEET_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / FP64_DATASHEET_TFLOPS, "traffic": traffic,
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        pass
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak_measured, "unit": "TFLOP/s",
+                "frac": achieved / peak_measured, "traffic": traffic,
+                "peak_source": "measured in this run: FP64 tensor pipe (DMMA.8x8x4) probe, 148 SMs x 16 warps x 8 "
+                               "independent chains, best of 3 (gemm_peak_probe; Eq. (8) P:259-262). "
+                               "MEASURED_PEAKS.json has no FP64 entry (DESIGN.md §Roofline)",
+                "peak_datasheet": FP64_DATASHEET_TFLOPS, "frac_of_datasheet": achieved / FP64_DATASHEET_TFLOPS,
                 "kernel": cfg_name, "kernel_ms_mean": k_mean, "flops_per_launch": flops_local,
                 "launches_per_gemm": launches_per_step,
                 # compulsory HBM bytes of one GEMM (A, B read once, C written once; beta = 0), for
                 # comparison with `traffic` (DESIGN.md §6 explains the gap: L2-sized waves)
-                "algorithmic_bytes": 8.0 * (Ml * K + K * N + Ml * N),
-                "peak_source": "FP64 / FP64-tensor datasheet peak of one HGX B200 GPU (296/8); MEASURED_PEAKS.json has "
-                               "no FP64 entry (DESIGN.md §Roofline)"}
+                "algorithmic_bytes": 8.0 * (Ml * K + K * N + Ml * N)}
     if peaks.get("bf16_tflops"):
         roofline["peak_bf16_scaled"] = peaks["bf16_tflops"] * FP64_DATASHEET_TFLOPS / BF16_NOMINAL_TFLOPS
     if clocks.get("sm_mhz"):
-        clk_peak = 148 * 128 * clocks["sm_mhz"] * 1e6 / 1e12
+        clk_peak = sms * 128 * clocks["sm_mhz"] * 1e6 / 1e12
         roofline["peak_at_run_clock"] = clk_peak
         roofline["frac_at_run_clock"] = achieved / clk_peak
 
     # ---- end to end through the host-buffer C-ABI call ------------------------------
     e2e = None
-    if a.workload == "large" and not a.no_e2e:
-        # 40 GiB of pinned host memory per rank (B alone is 32 GiB): not run by default
-        e2e = {"value": None, "unit": "TFLOP/s", "skipped": "large workload: 40 GiB pinned host buffers per rank"}
+    if a.workload in ("large", "large_strong") and not a.no_e2e:
+        # 40+ GiB of pinned host memory per rank (B alone is 32 GiB): not run by default
+        e2e = {"value": None, "unit": "TFLOP/s", "skipped": f"{a.workload} workload: >= 40 GiB pinned host buffers"}
     elif not a.no_e2e:
         try:
             e2e = run_e2e(a, G, dist, comm, stream, dA, dB, dC, M, N, K, Ml, world, flops_step)
@@ -416,23 +594,22 @@ def main():
                            "beta": 0.0, "inputs": "seeded uniform[-1,1) (synth generator, device fill)",
                            "l2": "inputs larger than L2 (no flush)", "kernel_cfg": cfg_name,
                            "parallelism": f"row-sharded x{world}, B broadcast (NCCL)" if world > 1 else "1 GPU",
-                           "bcast": bcast_via},
+                           "step": step_via},
                 "pct_of_fp64_peak": 100.0 * value / (FP64_DATASHEET_TFLOPS * world),
-                "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "clocks": clocks, "roofline": roofline, "parity": parity, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": a.steps * launches_per_step}
         if distributed:
-            # the one exchange step: B's broadcast runs on the same stream right
-            # before the GEMM, so its time per step is the step time minus the GEMM's
-            bc = max(0.0, t_ms / a.steps - k_mean)
-            line["exchange"] = {"op": "broadcast of B (NCCL)", "bytes_per_step": 8 * K * N,
-                                "ms_per_step": bc, "share_of_step": bc / (t_ms / a.steps),
-                                "algbw_GBs": (8 * K * N / (bc * 1e-3) / 1e9) if (bc > 0 and world > 1) else None}
+            # the one exchange step, timed alone after the timed region
+            line["exchange"] = {"op": "broadcast of B (NCCL)", "bytes_per_step": 8 * K * N, "ms_per_step": b_mean,
+                                "share_of_step": b_mean / (t_ms / a.steps),
+                                "gemm_ms": k_mean,
+                                "algbw_GBs": (8 * K * N / (b_mean * 1e-3) / 1e9) if (b_mean > 0 and world > 1) else None}
         print(json.dumps(line), flush=True)
     if comm is not None:
         comm.close()
     if distributed:
         dist.destroy_process_group()
-    return 0
+    return 0 if parity["ok"] else 1
 
 
 if __name__ == "__main__":

@@ -188,6 +188,12 @@ GEMM_API int gemm_cfg_select(int64_t M, int64_t N, int64_t K, const double *A, i
 GEMM_API int gemm_plan(int64_t M, int64_t N, int64_t K, const double *A, int64_t lda,
               const double *B, int64_t ldb, int *cfg_id, int *splits);
 
+/* gemm_plan, optionally restricted (one_pass != 0) to plans that run each tile's k-range in
+ * one pass (no split-K / stream-K / hybrid) -- the plan gemm_f64_ex(cfg_id = -1, splits = 1),
+ * gemm_f64_host's blocks and gemm_f64_sharded launch (*splits is then 1). */
+GEMM_API int gemm_plan_ex(int64_t M, int64_t N, int64_t K, const double *A, int64_t lda,
+                 const double *B, int64_t ldb, int one_pass, int *cfg_id, int *splits);
+
 /* Auto-tuner hooks (the paper's per-architecture tuning, §2.3, as a
  * persisted per-shape table).  gemm_plan_set pins the plan the heuristic entry
  * points use for (M, N, K, TMA-eligible) on every device; gemm_plan_clear
@@ -244,6 +250,10 @@ GEMM_API int gemm_comm_init(void **comm_out, int nranks, const unsigned char id[
 /* Destroys a communicator (NULL is a no-op).  Collective like ncclCommDestroy; the caller
  * must have synchronized the streams its calls used. */
 GEMM_API int gemm_comm_destroy(void *comm);
+/* The communicator's size and this process's rank as NCCL reports them (ncclCommCount,
+ * ncclCommUserRank): *nranks, *rank (caller-owned ints).  NULL -> GEMM_ERR_ARG; NCCL failure
+ * -> GEMM_ERR_NCCL.  bench.py logs it per rank. */
+GEMM_API int gemm_comm_info(void *comm, int *nranks, int *rank);
 
 /* Row-block-sharded GEMM (collective: every rank calls it with the same N, K,
  * alpha, beta, root).  Rank r owns rows [floor(r*M/P), floor((r+1)*M/P)) of A

@@ -32,6 +32,14 @@ static const CfgEntry k_table[] = {
     DG_SK(64, 64, 32, 16, 32, 3),
     DG_SK(128, 64, 32, 32, 32, 3),
     DG_TMA_SPLIT(128, 64, 32, 32, 32, 3),
+    // one 16-warp CTA per SM (E = 16): no co-resident CTA to share the DMMA pipe unevenly
+    DG_SK(128, 64, 32, 32, 16, 4),
+    DG_SK(64, 128, 32, 16, 32, 4),
+    DG_TMA_SPLIT(128, 64, 32, 32, 16, 4),
+    // persistent, dynamically scheduled split-K with per-warp partial publication
+    DG_PSK(64, 64, 32, 32, 16, 3),
+    DG_PSK(64, 64, 16, 32, 16, 6),
+    DG_PSK(128, 64, 32, 32, 16, 4),
 };
 
 const CfgEntry *cfg_table_small(int *n) {

@@ -525,6 +525,10 @@ int workspace_release_f64() {
 
 static int get_split_ws(cudaStream_t st, size_t doubles, size_t tiles, double **ws, int **ctr);
 
+int split_workspace(cudaStream_t st, size_t doubles, size_t counters, double **ws, int **ctr) {
+    return get_split_ws(st, doubles, counters, ws, ctr);
+}
+
 int streamk_workspace(cudaStream_t st, size_t slot_doubles, int grid, size_t tiles, double **ws, int **ctr) {
     return get_split_ws(st, slot_doubles * 2 * (size_t)grid, tiles, ws, ctr);
 }
@@ -822,6 +826,18 @@ int gemm_plan(int64_t M, int64_t N, int64_t K, const double *A, int64_t lda, con
     const Choice c = choose(M, N, K, tma_ok(A, lda, B, ldb));
     *cfg_id = c.id;
     *splits = c.splits;
+    return GEMM_OK;
+}
+
+int gemm_plan_ex(int64_t M, int64_t N, int64_t K, const double *A, int64_t lda, const double *B, int64_t ldb,
+                 int one_pass, int *cfg_id, int *splits) {
+    clear_error();
+    if (!cfg_id || !splits) return set_error(GEMM_ERR_ARG, "cfg_id / splits is NULL");
+    if (M == 1) lda += (lda & 1);
+    if (K == 1) ldb += (ldb & 1);
+    const Choice c = choose(M, N, K, tma_ok(A, lda, B, ldb), one_pass != 0);
+    *cfg_id = c.id;
+    *splits = one_pass ? 1 : c.splits;
     return GEMM_OK;
 }
 

@@ -108,6 +108,15 @@ int gemm_comm_destroy(void *comm) {
     return rc;
 }
 
+int gemm_comm_info(void *comm, int *nranks, int *rank) {
+    clear_error();
+    if (!comm || !nranks || !rank) return set_error(GEMM_ERR_ARG, "comm / nranks / rank is NULL");
+    Comm *c = static_cast<Comm *>(comm);
+    int rc = nccl_check(ncclCommCount(c->nccl, nranks), "ncclCommCount");
+    if (!rc) rc = nccl_check(ncclCommUserRank(c->nccl, rank), "ncclCommUserRank");
+    return rc;
+}
+
 int gemm_bcast_f64(double *buf, int64_t count, int root, void *comm, void *stream) {
     clear_error();
     if (!comm) return set_error(GEMM_ERR_ARG, "comm is NULL");

@@ -25,10 +25,10 @@ FILL_MODES = {"uniform": 0, "dyadic": 1, "int8": 2, "ones": 3, "identity": 4, "z
 EXPORTS = ("gemm_f64", "gemm_f64_stream", "gemm_f64_cfg", "gemm_f64_ex", "gemm_f32", "gemm_f32_stream",
            "gemm_f32_cfg", "gemm_f32_num_cfgs", "gemm_f32_cfg_name", "gemm_f64_host", "gemm_host_pool_release",
            "gemm_workspace_release",
-           "gemm_num_cfgs", "gemm_cfg_name", "gemm_cfg_info", "gemm_cfg_select", "gemm_plan", "gemm_plan_set",
+           "gemm_num_cfgs", "gemm_cfg_name", "gemm_cfg_info", "gemm_cfg_select", "gemm_plan", "gemm_plan_ex", "gemm_plan_set",
            "gemm_plan_clear", "gemm_tune_load", "gemm_last_error",
            "gemm_fill_f64", "gemm_peak_probe", "gemm_comm_unique_id", "gemm_comm_init",
-           "gemm_comm_destroy", "gemm_f64_sharded", "gemm_bcast_f64", "gemm_version")
+           "gemm_comm_destroy", "gemm_comm_info", "gemm_f64_sharded", "gemm_bcast_f64", "gemm_version")
 
 
 class GemmError(RuntimeError):
@@ -67,6 +67,7 @@ def _load():
         "gemm_cfg_info": (ci, [ci, ctypes.POINTER(CfgDesc)]),
         "gemm_cfg_select": (ci, [i64, i64, i64, vp, i64, vp, i64]),
         "gemm_plan": (ci, [i64, i64, i64, vp, i64, vp, i64, ctypes.POINTER(ci), ctypes.POINTER(ci)]),
+        "gemm_plan_ex": (ci, [i64, i64, i64, vp, i64, vp, i64, ci, ctypes.POINTER(ci), ctypes.POINTER(ci)]),
         "gemm_plan_set": (ci, [i64, i64, i64, ci, ci, ci]),
         "gemm_plan_clear": (ci, []),
         "gemm_tune_load": (ci, [ctypes.c_char_p, ctypes.POINTER(ci)]),
@@ -76,6 +77,7 @@ def _load():
         "gemm_comm_unique_id": (ci, [ctypes.c_char_p]),
         "gemm_comm_init": (ci, [ctypes.POINTER(vp), ci, ctypes.c_char_p, ci]),
         "gemm_comm_destroy": (ci, [vp]),
+        "gemm_comm_info": (ci, [vp, ctypes.POINTER(ci), ctypes.POINTER(ci)]),
         "gemm_f64_sharded": (ci, [i64, i64, i64, dbl, vp, i64, vp, i64, dbl, vp, i64, vp, ci, ci, vp]),
         "gemm_bcast_f64": (ci, [vp, i64, ci, vp, vp]),
         "gemm_version": (ctypes.c_char_p, []),
@@ -317,12 +319,27 @@ def cfg_select(M, N, K, A_ptr=0, lda=None, B_ptr=0, ldb=None) -> int:
                                 ldb if ldb is not None else max(N, 1))
 
 
-def plan(M, N, K, A_ptr=0, lda=None, B_ptr=0, ldb=None) -> tuple:
-    """(cfg_id, splits) the heuristic launches for this shape / alignment."""
+def plan(M, N, K, A_ptr=0, lda=None, B_ptr=0, ldb=None, one_pass: bool = False) -> tuple:
+    """(cfg_id, splits) the heuristic launches for this shape / alignment; one_pass=True: the
+    plan of gemm(..., splits=1), gemm_host's blocks and Comm.gemm_sharded (gemm_plan_ex)."""
     cid, sp = ctypes.c_int(), ctypes.c_int()
-    _check(_lib.gemm_plan(M, N, K, A_ptr, lda if lda is not None else max(K, 1), B_ptr,
-                          ldb if ldb is not None else max(N, 1), ctypes.byref(cid), ctypes.byref(sp)))
+    lda = lda if lda is not None else max(K, 1)
+    ldb = ldb if ldb is not None else max(N, 1)
+    if one_pass:
+        _check(_lib.gemm_plan_ex(M, N, K, A_ptr, lda, B_ptr, ldb, 1, ctypes.byref(cid), ctypes.byref(sp)))
+    else:
+        _check(_lib.gemm_plan(M, N, K, A_ptr, lda, B_ptr, ldb, ctypes.byref(cid), ctypes.byref(sp)))
     return cid.value, sp.value
+
+
+def sharded_panels(N: int, chunks: int) -> list:
+    """Column panels [(n0, width)] gemm_f64_sharded uses for bcast_chunks = chunks (mirrors
+    csrc/sharded.cu: at most N/64 panels, widths a multiple of 16 except the last)."""
+    nch = min(chunks, max(1, N // 64))
+    if nch <= 1:
+        return [(0, N)]
+    w = ((N + nch - 1) // nch + 15) // 16 * 16
+    return [(n0, min(N, n0 + w) - n0) for n0 in range(0, N, w)]
 
 
 HYB_MIN_STEPS = 16   # registry.cuh kHybMinSteps
@@ -399,6 +416,12 @@ class Comm:
     @property
     def handle(self):
         return self._h
+
+    def info(self) -> tuple:
+        """(nranks, rank) as NCCL reports them for this communicator (gemm_comm_info)."""
+        n, r = ctypes.c_int(), ctypes.c_int()
+        _check(_lib.gemm_comm_info(self._h, ctypes.byref(n), ctypes.byref(r)))
+        return n.value, r.value
 
     def bcast(self, X, root: int = 0, stream=None):
         _check(_lib.gemm_bcast_f64(X.data_ptr(), X.numel(), root, self._h, _stream_ptr(stream)))

@@ -1,7 +1,7 @@
 """Unified (managed) memory vs explicit device memory (PAPER.md P:216, P:892:
 "all GPUs show a better performance when using unified memory").
 
-    python tools/managed.py [--sizes 8192,16384] [--out gpurun_out/managed.json]
+    python tools/managed.py [--sizes 1024,2048,4096,8192,16384] [--out gpurun_out/managed.json]
 
 For each size, the same seeded DGEMM (alpha=1, beta=0) runs on
   device   : cudaMalloc buffers (torch), inputs generated on the GPU
@@ -9,8 +9,11 @@ For each size, the same seeded DGEMM (alpha=1, beta=0) runs on
   host-init: cudaMallocManaged buffers written by the CPU first, no prefetch (pages migrate on
              demand during the first launch)
   prefetch : like host-init, then cudaMemPrefetchAsync to the GPU before the launch
-and reports the first launch and the steady state (best of reps).  The managed results
-are checked bitwise against the device result (same plan, same per-entry arithmetic).
+and reports the first launch (one call between two events, right after the inputs were
+written) and the steady state: device time per call of back-to-back calls (the tuner's
+batched timing, so the ~10 us host cost per call overlaps the kernels at small N; best of
+reps).  The managed results are checked bitwise against the device result (same plan, same
+per-entry arithmetic); tests/test_gpu_managed.py checks them against the CPU oracle.
 """
 
 import argparse
@@ -76,6 +79,11 @@ def timed(fn):
     return e0.elapsed_time(e1) * 1e-3
 
 
+def steady(fn, reps):
+    from paper_1706_10086_b200 import tuner
+    return tuner._time(fn, reps)[0]
+
+
 def run(n, reps):
     fl = 2.0 * n ** 3
     nbytes = 8 * n * n
@@ -87,7 +95,7 @@ def run(n, reps):
     G.fill(A, "uniform", 1706, 0)
     G.fill(B, "uniform", 1706, 1)
     first = timed(lambda: gemm_raw(n, A.data_ptr(), B.data_ptr(), C.data_ptr()))
-    best = min(timed(lambda: gemm_raw(n, A.data_ptr(), B.data_ptr(), C.data_ptr())) for _ in range(reps))
+    best = steady(lambda: gemm_raw(n, A.data_ptr(), B.data_ptr(), C.data_ptr()), reps)
     out["device"] = {"first_tflops": fl / first / 1e12, "tflops": fl / best / 1e12}
     ref = C.cpu().numpy()
     del A, B, C
@@ -108,7 +116,7 @@ def run(n, reps):
         t0 = time.perf_counter()
         first = timed(lambda: gemm_raw(n, pa, pb, pc))
         wall_first = time.perf_counter() - t0
-        best = min(timed(lambda: gemm_raw(n, pa, pb, pc)) for _ in range(reps))
+        best = steady(lambda: gemm_raw(n, pa, pb, pc), reps)
         got = np.ctypeslib.as_array((ctypes_c_double * (n * n)).from_address(pc)).reshape(n, n).copy()
         out[mode] = {"first_tflops": fl / first / 1e12, "first_wall_s": wall_first, "tflops": fl / best / 1e12,
                      "bitwise_equal_to_device": bool(np.array_equal(got, ref))}
@@ -119,8 +127,8 @@ def run(n, reps):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--sizes", default="8192,16384")
-    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--sizes", default="1024,2048,4096,8192,16384")
+    ap.add_argument("--reps", type=int, default=7)
     ap.add_argument("--out", default="gpurun_out/managed.json")
     a = ap.parse_args()
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
