@@ -559,6 +559,42 @@ def test_cuda_graph_capture_and_replay(cuda_lib):
         assert np.array_equal(o.cpu().numpy(), eager)
 
 
+def test_cuda_graph_survives_workspace_growth(cuda_lib):
+    """a graph captured from a split-K call keeps pointing at the workspace it was
+    captured with.  A later eager call that needs a LARGER workspace on the same stream must
+    not free it (it is retired, not freed), so replaying the graph afterwards still gives the
+    eager bits; gemm_workspace_release() then frees everything and eager calls still work."""
+    n = 256
+    A, B, C0 = synth.problem(n, n, n, seed=22)
+    dA, dB = dev(A), dev(B)
+    out = torch.zeros((n, n), dtype=torch.float64, device="cuda")
+    s = torch.cuda.Stream()
+    sk = cuda_lib.cfg_id("tma_64x64x32_w32x16_s3_splitk")
+    with torch.cuda.stream(s):
+        cuda_lib.gemm(dA, dB, out, 1.0, 0.0, cfg=sk, splits=4)      # warm-up (workspace for 256^3 x4)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        cuda_lib.gemm(dA, dB, out, 1.0, 0.0, cfg=sk, splits=4)
+    # a much larger split-K call on the capture stream grows the workspace (old buffer retired)
+    big = 2048
+    bA = torch.ones((big, big), dtype=torch.float64, device="cuda")
+    bC = torch.zeros((big, big), dtype=torch.float64, device="cuda")
+    with torch.cuda.stream(s):
+        cuda_lib.gemm(bA, bA, bC, 1.0, 0.0, cfg=sk, splits=8)
+        torch.empty((big, big), dtype=torch.float64, device="cuda").fill_(np.nan)   # reuse freed memory, if any
+    torch.cuda.synchronize()
+    assert float(bC[7, 9]) == big
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    eager = run_gpu(cuda_lib, A, B, C0, 1.0, 0.0, cfg=sk, splits=4)
+    assert np.array_equal(out.cpu().numpy(), eager)
+    del g
+    cuda_lib.workspace_release()
+    assert np.array_equal(run_gpu(cuda_lib, A, B, C0, 1.0, 0.0, cfg=sk, splits=4), eager)
+
+
 # ---------------------------------------------------------------- hybrid (row a5)
 HYBRID_SHAPES = [
     (1024, 2368, 64),     # T = 148 tiles = one full wave, no tail
