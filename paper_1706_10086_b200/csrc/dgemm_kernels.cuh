@@ -220,6 +220,14 @@ __device__ __forceinline__ void epilogue(const double (&acc)[C::MB][C::NP][2][2]
     }
 }
 
+// floor(a * b / c) for 0 <= a, b and 0 < c: a 32-bit division when the product fits (always,
+// for k-step ranges), the 64-bit one only otherwise
+__device__ __forceinline__ int mul_div(int a, int b, int c) {
+    const unsigned long long p = (unsigned long long)(unsigned)a * (unsigned)b;
+    if (p <= 0xffffffffull) return (int)((unsigned)p / (unsigned)c);
+    return (int)(p / (unsigned long long)c);
+}
+
 // Grouped raster (row a1): consecutive CTAs walk group_m tile-rows column by column.
 __device__ __forceinline__ void tile_coords(int bid, int tiles_m, int tiles_n, int group_m, int &tm, int &tn) {
     const int per_group = group_m * tiles_n;
@@ -717,19 +725,22 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
     // other 255 threads no registers (the E = 16 instances live within 128 per thread)
     struct Prod {
         uint64_t pol;   // L2 policy, created once
-        int unit, k, k1, tm, tn, done;
+        int tile, slice, k, k1, tm, tn, done;
     };
     __shared__ Prod ps;
+    // unit -> (tile, slice, k-range, tile coordinates): 32-bit divisions only (a 64-bit one is a
+    // long software sequence on the refilling warp's path; per-CTA traces showed it in the fill)
     auto start_unit = [&](int u) {
         if (u >= U) {
             ps.done = 1;
             if (u == U + (int)gridDim.x - 1) atomicExch(pk.queue, 0);   // last ticket of the launch
             return;
         }
-        ps.unit = u;
         const int t = u / S, sl = u - t * S;
-        ps.k = (int)(((int64_t)sl * KT) / S);
-        ps.k1 = (int)(((int64_t)(sl + 1) * KT) / S);
+        ps.tile = t;
+        ps.slice = sl;
+        ps.k = mul_div(sl, KT, S);
+        ps.k1 = mul_div(sl + 1, KT, S);
         int tm, tn;
         tile_coords(t, tiles_m, tiles_n, group_m, tm, tn);
         ps.tm = tm;
@@ -742,9 +753,9 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
             mbar_arrive(&full[slot]);   // completes the phase without data: consumers stop here
             return;
         }
-        const int k = ps.k, unit = ps.unit;
+        const int k = ps.k;
         const bool last = (k + 1 == ps.k1);
-        info[slot] = make_int4(unit / S, unit % S, 0, last ? 1 : 0);
+        info[slot] = make_int4(ps.tile, ps.slice, 0, last ? 1 : 0);
         tma_issue_stage<C>(base_ptr + slot * C::STAGE_BYTES, &tmA, &tmB, &full[slot], ps.tm * C::BM, ps.tn * C::BN,
                            k, ps.pol);
         ps.k = k + 1;
@@ -764,12 +775,12 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
         tma_prefetch_desc(&tmB);
         ps.done = 0;
         ps.pol = l2_policy_evict_normal();
+        start_unit(blockIdx.x);   // the first unit is static (grid <= U): set up before the wait
     }
     griddep_wait();
     DG_TRACE_AT(1);
     griddep_launch();
     if (producer) {
-        start_unit(blockIdx.x);   // the first unit is static (grid <= U): no atomic before the fill
         for (int s = 0; s < C::STAGES; ++s) issue_next(s);
     }
     __syncthreads();
@@ -784,14 +795,21 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
 #pragma unroll
             for (int j = 0; j < 2; ++j) acc[mb][np][j][0] = acc[mb][np][j][1] = 0.0;
 
+    // The refill of the slot released at it - 1 is issued by lane 0 of warp it % R: a refill
+    // (ten TMA issues, the unit bookkeeping, a ticket claim at unit ends) costs the issuing warp
+    // a few hundred cycles ahead of its DMMAs; one fixed producer warp became the laggard of
+    // every stage (consumers stalled on `full`, ncu: 18 % of warp samples, profiles/r02).  The
+    // producer state in `ps` is handed from warp to warp by the ring itself: warp it % R reads
+    // it only after the empty barrier of slot it - 1, i.e. after the previous refiller's release.
+    constexpr int R = 4 < C::CONSUMER_WARPS ? 4 : C::CONSUMER_WARPS;
     int stage = 0, phase = 0;
     for (int it = 0;; ++it) {
-        if (producer && it > 0) {   // refill the slot released at it - 1 (the one before `stage`)
+        if (it > 0 && lane == 0 && warp == it % R) {   // refill the slot released at it - 1
             const int sp = stage == 0 ? C::STAGES - 1 : stage - 1;
             mbar_wait(&empty[sp], (uint32_t)(stage == 0 ? phase ^ 1 : phase));
             issue_next(sp);
         }
-        __syncwarp();   // the producer lane rejoins before the warp-wide mma.sync
+        __syncwarp();   // the refilling lane rejoins before the warp-wide mma.sync
         mbar_wait(&full[stage], (uint32_t)phase);
         const int4 in = info[stage];
         if (in.x < 0) break;
