@@ -40,6 +40,10 @@ static const CfgEntry k_table[] = {
     DG_PSK(64, 64, 32, 32, 16, 3),
     DG_PSK(64, 64, 16, 32, 16, 6),
     DG_PSK(128, 64, 32, 32, 16, 4),
+    // cluster split-K: the slices of a tile reduce through distributed shared memory
+    DG_CSK(64, 64, 32, 32, 16, 3),
+    DG_CSK(64, 64, 16, 32, 16, 6),
+    DG_CSK(128, 64, 32, 32, 32, 3),
 };
 
 const CfgEntry *cfg_table_small(int *n) {

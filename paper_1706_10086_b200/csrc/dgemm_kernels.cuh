@@ -363,6 +363,53 @@ __device__ __forceinline__ bool split_reduce(double (&acc)[C::MB][C::NP][2][2], 
     return partial_reduce<C>(acc, sk.ws, sk.counters, tile, sk.splits, s, sk.splits, warp, lane);
 }
 
+// Cluster split-K (SPLIT == 2, row a5): the S = gridDim.y slices of a tile run as one thread-
+// block cluster (1, S, 1).  After its k-range each CTA writes its raw partial into its own
+// shared memory (the drained ring), the cluster synchronises, and CTA s reduces the 256-bit
+// accumulator groups q = s, s + S, ... of every thread: it reads group q of the same thread
+// from the S CTAs through distributed shared memory in slice order 0..S-1 -- the order, and so
+// the bits, of the global-memory split-K with the same S -- and stores those C quads.  No
+// global partials, no counters, no last-arriver: the reduction is spread evenly over the
+// cluster's CTAs.  A second cluster barrier keeps every CTA's shared memory alive until the
+// others have read it.
+template <class C>
+__device__ __forceinline__ void cluster_reduce_epilogue(double (&acc)[C::MB][C::NP][2][2], uint32_t part, int warp,
+                                                        int lane, int row0, int col0, int M, int N, double alpha,
+                                                        double beta, double *__restrict__ Cm, int64_t ldc, bool vec) {
+    constexpr int Q = C::E / 4;
+    static_assert(C::STAGES * C::STAGE_BYTES >= (uint32_t)C::E * C::CONSUMER_THREADS * 8, "partial fits the ring");
+    const double *flat = &acc[0][0][0][0];
+    // partial layout [q][warp][lane][4 doubles]: a warp's 32 lanes write 1 KB contiguously
+    __syncthreads();   // every warp has finished reading the ring's last stage
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const uint32_t a = part + (uint32_t)(((q * C::CONSUMER_WARPS + warp) * 32 + lane) * 32);
+        sts_v2(a, flat[4 * q], flat[4 * q + 1]);
+        sts_v2(a + 16, flat[4 * q + 2], flat[4 * q + 3]);
+    }
+    dsm_sync();
+    const int S = (int)gridDim.y;   // cluster size
+    const int me = (int)dsm_rank();
+    for (int q = me; q < Q; q += S) {
+        const uint32_t a = part + (uint32_t)(((q * C::CONSUMER_WARPS + warp) * 32 + lane) * 32);
+        double x[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int s = 0; s < S; ++s) {   // slice order
+            const uint32_t r = dsm_map(a, (uint32_t)s);
+            double v0, v1, v2, v3;
+            dsm_ld_v2(r, v0, v1);
+            dsm_ld_v2(r + 16, v2, v3);
+            x[0] += v0;
+            x[1] += v1;
+            x[2] += v2;
+            x[3] += v3;
+        }
+        const int mb = q / C::NP, np = q - mb * C::NP;
+        const double w[4] = {x[0], x[2], x[1], x[3]};   // (j,i) = (0,0), (1,0), (0,1), (1,1)
+        epilogue_quad(w, row0 + mb * 8, col0 + np * 16, M, N, alpha, beta, Cm, ldc, vec);
+    }
+    dsm_sync();
+}
+
 // SPLIT = false instantiations carry no split-K code (the reduction's registers would
 // otherwise raise the 256x64/64x32 kernel from 199 to 255 registers).
 // XP = true: cross-stage fragment prefetch -- the first half of stage i+1 is loaded (after
@@ -371,7 +418,7 @@ __device__ __forceinline__ bool split_reduce(double (&acc)[C::MB][C::NP][2][2], 
 // ROT > 1: the refill of k-step i is issued by lane 0 of warp i % ROT instead of always by
 // warp 0, spreading the producer's per-k-step instructions over ROT warps (and so over the
 // SM's sub-partitions); the ring protocol is unchanged.
-template <class C, bool SPLIT, bool XP, int ROT = 1>
+template <class C, int SPLIT, bool XP, int ROT = 1>
 __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
     dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
                      int N, int K, double alpha, double beta, double *__restrict__ Cm, int64_t ldc, int vec,
@@ -391,7 +438,7 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int KT = (K + C::BK - 1) / C::BK;
     const int split = SPLIT ? (int)blockIdx.y : 0;
-    const int nsplit = SPLIT ? sk.splits : 1;
+    const int nsplit = SPLIT == 2 ? (int)gridDim.y : (SPLIT ? sk.splits : 1);
     const int kt0 = (int)(((int64_t)split * KT) / nsplit);
     const int NK = (int)(((int64_t)(split + 1) * KT) / nsplit) - kt0;   // k-steps of this CTA
     const bool producer = (threadIdx.x == 0);
@@ -495,7 +542,14 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
 #ifdef DG_TRACE
     DG_TRACE_SLOT(7, (unsigned long long)dg_smid());
 #endif
-    if constexpr (SPLIT) {
+    if constexpr (SPLIT == 2) {
+        if (gridDim.y > 1) {
+            cluster_reduce_epilogue<C>(acc, base, warp, lane, m0 + warp_m * C::WM + (lane >> 2),
+                                       n0 + warp_n * C::WN + 4 * (lane & 3), M, N, alpha, beta, Cm, ldc, vec != 0);
+            DG_TRACE_AT(6);
+            return;
+        }
+    } else if constexpr (SPLIT == 1) {
         if (!split_reduce<C>(acc, sk, blockIdx.x, split, warp, lane)) {
             DG_TRACE_AT(6);
             return;

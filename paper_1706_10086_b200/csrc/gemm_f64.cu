@@ -388,7 +388,8 @@ static Choice choose_uncached(int64_t M, int64_t N, int64_t K, bool tma, bool si
             }
             continue;
         }
-        const int smax = (d.split_k == 1 || single_pass) ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(16, KT / 2));
+        const int64_t scap = d.split_k == -3 ? 8 : 16;   // cluster split-K: portable cluster size
+        const int smax = (d.split_k == 1 || single_pass) ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(scap, KT / 2));
         for (int S = 1; S <= smax; ++S) {
             const double t = est_time(d, occ, sms, M, N, K, S, c.eff);
             if (t < best_t * 0.999) {
@@ -437,7 +438,8 @@ static int auto_splits(int id, int64_t M, int64_t N, int64_t K) {
     const gemm_cfg_desc &d = g_cfgs[id].d;
     if (d.split_k > 1) return d.split_k;
     const int64_t KT = (K + d.bk - 1) / d.bk;
-    const int smax = (int)std::max<int64_t>(1, std::min<int64_t>(16, KT / 2));
+    const int64_t scap = d.split_k == -3 ? 8 : 16;   // cluster split-K: portable cluster size
+    const int smax = (int)std::max<int64_t>(1, std::min<int64_t>(scap, KT / 2));
     int bestS = 1;
     double bt = 1e300;
     for (int S = 1; S <= smax; ++S) {
@@ -693,13 +695,17 @@ int gemm_impl(int64_t M, int64_t N, int64_t K, double alpha, const double *A, in
     rc = prepare_cfg(id, &occ);
     if (rc) return rc;
     const gemm_cfg_desc &d = g_cfgs[id].d;
-    if (cfg_id >= 0 && d.split_k == 0) splits = force_splits > 0 ? force_splits : auto_splits(id, M, N, K);
-    if (d.split_k < 0) splits = 1;   // stream-K / hybrid: the work split is fixed by the grid, not by S
-    if (force_splits > 1 && d.split_k != 0)
+    const bool cluster = (d.split_k == -3);   // cluster split-K: S per call, no workspace
+    if (cfg_id >= 0 && (d.split_k == 0 || cluster))
+        splits = force_splits > 0 ? force_splits : auto_splits(id, M, N, K);
+    if (d.split_k < 0 && !cluster) splits = 1;   // stream-K / hybrid: the work split is fixed by the grid
+    if (force_splits > 1 && d.split_k != 0 && !cluster)
         return set_error(GEMM_ERR_UNSUPPORTED, "cfg %s has no split-K (use a *_splitk configuration)", g_cfgs[id].name);
     if (splits > 4096) return set_error(GEMM_ERR_ARG, "splits=%d > 4096", splits);
     SplitArgs sk{1, nullptr, nullptr};
-    if (splits > 1) {
+    if (cluster) {
+        sk.splits = splits;   // reduced in distributed shared memory: no global workspace
+    } else if (splits > 1) {
         const size_t tiles = (size_t)((M + d.bm - 1) / d.bm) * (size_t)((N + d.bn - 1) / d.bn);
         rc = get_split_ws(st, tiles * (size_t)splits * d.bm * d.bn, tiles, &sk.ws, &sk.counters);
         if (rc) return rc;

@@ -83,6 +83,30 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 }
 
+// ---- thread-block clusters / distributed shared memory (cluster split-K) -------------------
+__device__ __forceinline__ uint32_t dsm_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
+}
+// every thread of every CTA of the cluster: release this CTA's prior shared-memory writes,
+// acquire the other CTAs'
+__device__ __forceinline__ void dsm_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// the address of the same shared-memory location in cluster CTA `rank`
+__device__ __forceinline__ uint32_t dsm_map(uint32_t smem_addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(smem_addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void dsm_ld_v2(uint32_t cluster_addr, double &x, double &y) {
+    asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];\n" : "=d"(x), "=d"(y) : "r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void sts_v2(uint32_t addr, double x, double y) {
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(addr), "d"(x), "d"(y) : "memory");
+}
+
 // ---- programmatic dependent launch (PDL) -------------------------------------------
 // The host launches every GEMM kernel with programmatic stream serialization, so a kernel
 // may become resident while the previous kernel in the stream is still draining.  Each

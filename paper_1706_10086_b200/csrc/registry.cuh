@@ -39,7 +39,7 @@ struct CfgEntry {
 // TMA kernels: the refill of k-step i is issued by warp i % kRotXP (dgemm_tma_kernel ROT)
 constexpr int kRotXP = 4;
 
-template <class C, bool SPLIT, bool XP, int ROT = 1>
+template <class C, int SPLIT, bool XP, int ROT = 1>
 static int launch_tma(const LaunchArgs &a, cudaStream_t st) {
     CUtensorMap ta, tb;
     int rc = make_tmap(&ta, a.A, a.M, a.K, a.lda, C::BM);
@@ -52,6 +52,26 @@ static int launch_tma(const LaunchArgs &a, cudaStream_t st) {
     return cuda_check(launch_k(dgemm_tma_kernel<C, SPLIT, XP, ROT>, grid, dim3(C::CONSUMER_THREADS), C::SMEM_BYTES, st,
                                ta, tb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec, a.group_m, a.sk),
                       "dgemm_tma_kernel launch");
+}
+
+// Cluster split-K: grid (tiles, S), clusters of (1, S, 1); S clamped to [1, min(8, KT)] (the
+// portable cluster size, at least one k-step per slice); S = 1 is the plain one-pass kernel.
+template <class C>
+static int launch_tma_cluster(const LaunchArgs &a, cudaStream_t st) {
+    CUtensorMap ta, tb;
+    int rc = make_tmap(&ta, a.A, a.M, a.K, a.lda, C::BM);
+    if (rc) return rc;
+    rc = make_tmap(&tb, a.B, a.K, a.N, a.ldb, 16);
+    if (rc) return rc;
+    const int64_t tiles = ((int64_t)a.M + C::BM - 1) / C::BM * (((int64_t)a.N + C::BN - 1) / C::BN);
+    if (tiles > 0x7FFFFFFF) return set_error(GEMM_ERR_UNSUPPORTED, "too many tiles (%lld)", (long long)tiles);
+    const int64_t KT = ((int64_t)a.K + C::BK - 1) / C::BK;
+    const int S = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(a.sk.splits, 8), KT));
+    SplitArgs none{1, nullptr, nullptr};
+    return cuda_check(launch_k_cluster(dgemm_tma_kernel<C, 2, false, kRotXP>, dim3((unsigned)tiles, S),
+                                       dim3(C::CONSUMER_THREADS), C::SMEM_BYTES, st, 1u, (unsigned)S, ta, tb, a.M,
+                                       a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec, a.group_m, none),
+                      "dgemm_tma_kernel (cluster split-K) launch");
 }
 
 template <class C>
@@ -183,6 +203,14 @@ static int launch_hybrid(const LaunchArgs &a, cudaStream_t st) {
                            (int)Cfg<BM, BN, BK, WM, WN, ST>::SMEM_BYTES, 1, -1, 0},                           \
              (const void *)dgemm_streamk_kernel<Cfg<BM, BN, BK, WM, WN, ST>>,                                 \
              launch_streamk<Cfg<BM, BN, BK, WM, WN, ST>>}
+
+// cluster split-K: split_k = -3 (slices chosen per call, reduced through distributed shared memory)
+#define DG_CSK(BM, BN, BK, WM, WN, ST)                                                                    \
+    CfgEntry{"tma_" #BM "x" #BN "x" #BK "_w" #WM "x" #WN "_s" #ST "_csplit",                                  \
+             gemm_cfg_desc{BM, BN, BK, WM, WN, ST, Cfg<BM, BN, BK, WM, WN, ST>::CONSUMER_THREADS,              \
+                           (int)Cfg<BM, BN, BK, WM, WN, ST>::SMEM_BYTES, 1, -3, 0},                           \
+             (const void *)dgemm_tma_kernel<Cfg<BM, BN, BK, WM, WN, ST>, 2, false, kRotXP>,                   \
+             launch_tma_cluster<Cfg<BM, BN, BK, WM, WN, ST>>}
 
 // persistent split-K: split_k = 0 (slices chosen per call, like *_splitk), one launch
 #define DG_PSK(BM, BN, BK, WM, WN, ST)                                                                    \

@@ -34,12 +34,13 @@ def candidates(M: int, N: int, K: int, tma: bool = True):
     for info in G.cfgs():
         if bool(info["tma"]) != tma:
             continue
-        if info["split_k"] != 0:
+        if info["split_k"] not in (0, -3):   # plain, stream-K, hybrid: the split is not per call
             out.append((info["id"], 1))
-        else:
+        else:                                # split-K (global partials) / cluster split-K (<= 8)
             kt = (K + info["bk"] - 1) // info["bk"]
+            smax = 8 if info["split_k"] == -3 else 16
             for s in (1, 2, 3, 4, 6, 8, 12, 16):
-                if s == 1 or (s <= kt // 2 and tiles_small * s <= 8 * 148 * 2):
+                if s == 1 or (s <= min(smax, kt // 2) and tiles_small * s <= 8 * 148 * 2):
                     out.append((info["id"], s))
     return out
 

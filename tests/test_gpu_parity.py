@@ -684,6 +684,7 @@ def test_hybrid_plan_full_size_tail_rows(cuda_lib, shape):
                                              ("tma_64x64x16_w32x16_s6_hybrid", None),
                                              ("tma_128x64x16_w32x16_s6_streamk", None),
                                              ("tma_64x64x32_w32x16_s3_persist", 1), ("tma_64x64x32_w32x16_s3_persist", 4),
+                                             ("tma_64x64x32_w32x16_s3_csplit", 4), ("tma_64x64x16_w32x16_s6_csplit", 8),
                                              ("tma_128x64x32_w32x16_s4_persist", 3)])
 def test_ring_slot_reuse_exact_k_signature(cuda_lib, cfg_name, splits):
     """Regression for the ring's write-after-read hazard (DESIGN.md §6 "Releasing a slot"):
@@ -748,3 +749,41 @@ def test_persist_uniform_within_bound_deterministic_and_counters_reset(cuda_lib)
             assert np.array_equal(out, first[S]), (cuda_lib.cfg_name(cfg), it, S)
         plain = run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=cuda_lib.cfg_id("tma_64x64x32_w16x32_s3"))
         assert np.array_equal(first[1], plain), cuda_lib.cfg_name(cfg)
+
+
+# ---------------------------------------------------------------- cluster split-K (row a5)
+def cluster_cfgs(G):
+    return [c["id"] for c in G.cfgs() if c["split_k"] == -3]
+
+
+@pytest.mark.parametrize("shape", [(64, 64, 64), (256, 256, 256), (130, 1000, 96), (1024, 1024, 1024), (520, 390, 1000),
+                                   (33, 18, 778)], ids=lambda s: "x".join(map(str, s)))
+def test_cluster_split_k_equals_global_split_k_bitwise(cuda_lib, shape):
+    """Cluster split-K sums the S slice partials in slice order through distributed shared
+    memory -- the same order as the global-memory split-K -- so for every S <= 8 the bits equal
+    the *_splitk kernel of the same tile with the same S (uniform inputs, alpha=1.5, beta=0.5),
+    and the result is within the bound and repeatable."""
+    M, N, K = shape
+    A, B, C0 = synth.problem(M, N, K, seed=M + 2 * N + K)
+    pairs = {"tma_64x64x32_w32x16_s3_csplit": "tma_64x64x32_w32x16_s3_splitk",
+             "tma_64x64x16_w32x16_s6_csplit": "tma_64x64x16_w32x16_s6_splitk"}
+    for cname, gname in pairs.items():
+        c, g = cuda_lib.cfg_id(cname), cuda_lib.cfg_id(gname)
+        kt = -(-K // cuda_lib.cfg_info(c)["bk"])
+        for S in (1, 2, 3, 4, 5, 8):
+            if S > kt:
+                continue
+            got = run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=c, splits=S)
+            ref = run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=g, splits=S)
+            assert np.array_equal(got, ref), (cname, S)
+            assert np.array_equal(got, run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=c, splits=S)), (cname, S)
+        check_vs_oracle(got, A, B, C0, 1.5, 0.5)
+
+
+def test_cluster_split_k_exact_regime_every_cfg(cuda_lib):
+    A, B, C0 = synth.problem(700, 650, 1300, mode="dyadic", seed=9)
+    ref = oracle.dgemm(1.5, A, B, 0.5, C0)
+    for cfg in cluster_cfgs(cuda_lib):
+        for S in (2, 4, 7, 8, 16):   # 16 is clamped to the portable cluster size 8
+            assert np.array_equal(run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=cfg, splits=S), ref), \
+                (cuda_lib.cfg_name(cfg), S)

@@ -27,7 +27,9 @@ def test_candidates_cover_tma_cfgs_and_split_counts(T):
     ids = {cid for cid, _ in c}
     assert {i["id"] for i in G.cfgs() if i["tma"]} == ids
     assert any(s > 1 for _, s in c)
-    assert all(s == 1 for cid, s in c if G.cfg_info(cid)["split_k"] != 0)
+    assert all(s == 1 for cid, s in c if G.cfg_info(cid)["split_k"] not in (0, -3))
+    assert all(s <= 8 for cid, s in c if G.cfg_info(cid)["split_k"] == -3)   # cluster split-K: portable size
+    assert any(s > 1 for cid, s in c if G.cfg_info(cid)["split_k"] == -3)
     assert all(not G.cfg_info(i)["tma"] for i, _ in T.candidates(64, 64, 64, tma=False))
 
 
