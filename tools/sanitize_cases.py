@@ -28,7 +28,7 @@ def main():
         G.fill(B, "uniform", 1, 1)
         G.fill(C, "uniform", 1, 2)
         for info in G.cfgs():
-            for s in ((1,) if info["split_k"] != 0 else (1, 3)):
+            for s in ((1,) if info["split_k"] not in (0, -3) else (1, 3)):   # split-K, persistent, cluster
                 G.gemm(A, B, C, 1.5, 0.5, cfg=info["id"], splits=s)
                 n += 1
         G.gemm(A, B, C, 0.0, 0.5)            # scale path
