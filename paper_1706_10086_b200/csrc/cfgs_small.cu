@@ -36,10 +36,6 @@ static const CfgEntry k_table[] = {
     DG_SK(128, 64, 32, 32, 16, 4),
     DG_SK(64, 128, 32, 16, 32, 4),
     DG_TMA_SPLIT(128, 64, 32, 32, 16, 4),
-    // persistent, dynamically scheduled split-K with per-warp partial publication
-    DG_PSK(64, 64, 32, 32, 16, 3),
-    DG_PSK(64, 64, 16, 32, 16, 6),
-    DG_PSK(128, 64, 32, 32, 16, 4),
     // cluster split-K: the slices of a tile reduce through distributed shared memory
     DG_CSK(64, 64, 32, 32, 16, 3),
     DG_CSK(64, 64, 16, 32, 16, 6),

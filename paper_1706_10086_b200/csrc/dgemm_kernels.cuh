@@ -220,14 +220,6 @@ __device__ __forceinline__ void epilogue(const double (&acc)[C::MB][C::NP][2][2]
     }
 }
 
-// floor(a * b / c) for 0 <= a, b and 0 < c: a 32-bit division when the product fits (always,
-// for k-step ranges), the 64-bit one only otherwise
-__device__ __forceinline__ int mul_div(int a, int b, int c) {
-    const unsigned long long p = (unsigned long long)(unsigned)a * (unsigned)b;
-    if (p <= 0xffffffffull) return (int)((unsigned)p / (unsigned)c);
-    return (int)(p / (unsigned long long)c);
-}
-
 // Grouped raster (row a1): consecutive CTAs walk group_m tile-rows column by column.
 __device__ __forceinline__ void tile_coords(int bid, int tiles_m, int tiles_n, int group_m, int &tm, int &tn) {
     const int per_group = group_m * tiles_n;
@@ -723,201 +715,6 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
     DG_TRACE_AT(6);
 #ifdef DG_TRACE
     DG_TRACE_SLOT(7, (unsigned long long)dg_smid() | ((unsigned long long)(tile - u0 / KT) << 32));
-#endif
-}
-
-// ------------------------------------------------------------------------------
-// Persistent, dynamically scheduled split-K (row a5, small and mid-size shapes).
-// U = tiles x S work units (unit u = slice u % S of tile u / S, k-steps
-// [s*KT/S, (s+1)*KT/S)).  A grid of G = SMs x resident CTAs pulls units from a global
-// ticket counter; lane 0 of warp 0 (the producer) streams the k-steps of its units through
-// the smem ring back to back, so the next unit's first stages are loading while the warps
-// finish the current one (no per-CTA pipeline fill per unit).  Each stage carries its unit in
-// smem (`info`, published with the stage's full barrier).  The two costs the per-CTA trace
-// showed for split-K CTAs -- the fill of every CTA and the whole-CTA barrier + fence +
-// last-arriver reduction at its end -- are replaced by:
-//  * per-WARP partial publication: a warp stores its sub-tile of the slice's partial, fences
-//    and bumps the (tile, warp) counter; the warp that completes a sub-tile (the S-th
-//    arrival) sums the S partials in slice order s = 0..S-1 (deterministic, independent of
-//    which CTA ran which slice) and writes C.  No CTA-wide barrier: the other warps go on
-//    with the next unit's k-steps, which the ring already holds.
-//  * S = 1: the warp's epilogue writes C directly (persistent data-parallel).
-// CTA g starts with unit g (grid <= U) and claims unit G + atomicAdd(queue, 1) for each next
-// one, when its producer has issued the current unit's last k-step.  Every CTA makes exactly
-// one failing claim (>= U), so claims G .. U + G - 1 are handed out and the CTA holding the
-// last one resets the counter for the next launch.  The
-// (tile, warp) counters are reset by the summing warp.
-struct PskArgs {
-    int splits;     // S >= 1
-    double *ws;     // [tiles * S][E/4][warps][32][4] partials (S > 1)
-    int *counters;  // [tiles * warps] (S > 1), zero between launches
-    int *queue;     // ticket counter, zero between launches
-};
-
-template <class C>
-__global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
-    dgemm_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
-                         int N, int K, double alpha, double beta, double *__restrict__ Cm, int64_t ldc, int vec,
-                         int group_m, PskArgs pk) {
-    extern __shared__ uint8_t smem_raw[];
-    const uint32_t raw = smem_u32(smem_raw);
-    const uint32_t base = (raw + 1023u) & ~1023u;
-    uint8_t *base_ptr = smem_raw + (base - raw);
-    uint64_t *full = reinterpret_cast<uint64_t *>(base_ptr + C::STAGES * C::STAGE_BYTES);
-    uint64_t *empty = full + C::STAGES;
-    __shared__ int4 info[C::STAGES];   // per stage: {tile, slice, -, last k-step of the unit}
-    DG_TRACE_AT(0);
-
-    const int tiles_m = (M + C::BM - 1) / C::BM, tiles_n = (N + C::BN - 1) / C::BN;
-    const int KT = (K + C::BK - 1) / C::BK;
-    const int S = pk.splits;
-    const int U = tiles_m * tiles_n * S;   // host: < 2^31 - gridDim.x
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const bool producer = (threadIdx.x == 0);
-
-    // producer state, touched by thread 0 only; kept in shared memory so that it costs the
-    // other 255 threads no registers (the E = 16 instances live within 128 per thread)
-    struct Prod {
-        uint64_t pol;   // L2 policy, created once
-        int tile, slice, k, k1, tm, tn, done;
-    };
-    __shared__ Prod ps;
-    // unit -> (tile, slice, k-range, tile coordinates): 32-bit divisions only (a 64-bit one is a
-    // long software sequence on the refilling warp's path; per-CTA traces showed it in the fill)
-    auto start_unit = [&](int u) {
-        if (u >= U) {
-            ps.done = 1;
-            if (u == U + (int)gridDim.x - 1) atomicExch(pk.queue, 0);   // last ticket of the launch
-            return;
-        }
-        const int t = u / S, sl = u - t * S;
-        ps.tile = t;
-        ps.slice = sl;
-        ps.k = mul_div(sl, KT, S);
-        ps.k1 = mul_div(sl + 1, KT, S);
-        int tm, tn;
-        tile_coords(t, tiles_m, tiles_n, group_m, tm, tn);
-        ps.tm = tm;
-        ps.tn = tn;
-    };
-    // fill ring slot `slot` with the next k-step of the ticket stream (or the end sentinel)
-    auto issue_next = [&](int slot) {
-        if (ps.done) {
-            info[slot] = make_int4(-1, 0, 0, 0);
-            mbar_arrive(&full[slot]);   // completes the phase without data: consumers stop here
-            return;
-        }
-        const int k = ps.k;
-        const bool last = (k + 1 == ps.k1);
-        info[slot] = make_int4(ps.tile, ps.slice, 0, last ? 1 : 0);
-        tma_issue_stage<C>(base_ptr + slot * C::STAGE_BYTES, &tmA, &tmB, &full[slot], ps.tm * C::BM, ps.tn * C::BN,
-                           k, ps.pol);
-        ps.k = k + 1;
-        // the next unit is claimed only now, STAGES - 1 k-steps before the warps finish this one:
-        // claiming earlier would let a CTA hold a unit it cannot start before others run dry
-        if (last) start_unit((int)gridDim.x + atomicAdd(pk.queue, 1));
-    };
-
-    if (producer) {
-#pragma unroll
-        for (int s = 0; s < C::STAGES; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], C::CONSUMER_WARPS);
-        }
-        fence_mbar_init();
-        tma_prefetch_desc(&tmA);
-        tma_prefetch_desc(&tmB);
-        ps.done = 0;
-        ps.pol = l2_policy_evict_normal();
-        start_unit(blockIdx.x);   // the first unit is static (grid <= U): set up before the wait
-    }
-    griddep_wait();
-    DG_TRACE_AT(1);
-    griddep_launch();
-    if (producer) {
-        for (int s = 0; s < C::STAGES; ++s) issue_next(s);
-    }
-    __syncthreads();
-
-    const int warp_m = warp / C::WARPS_N, warp_n = warp % C::WARPS_N;
-    const FragOffsets<C> fo(warp_m, warp_n, lane);
-    double acc[C::MB][C::NP][2][2];
-#pragma unroll
-    for (int mb = 0; mb < C::MB; ++mb)
-#pragma unroll
-        for (int np = 0; np < C::NP; ++np)
-#pragma unroll
-            for (int j = 0; j < 2; ++j) acc[mb][np][j][0] = acc[mb][np][j][1] = 0.0;
-
-    // The refill of the slot released at it - 1 is issued by lane 0 of warp it % R: a refill
-    // (ten TMA issues, the unit bookkeeping, a ticket claim at unit ends) costs the issuing warp
-    // a few hundred cycles ahead of its DMMAs; one fixed producer warp became the laggard of
-    // every stage (consumers stalled on `full`, ncu: 18 % of warp samples, profiles/r02).  The
-    // producer state in `ps` is handed from warp to warp by the ring itself: warp it % R reads
-    // it only after the empty barrier of slot it - 1, i.e. after the previous refiller's release.
-    constexpr int R = 4 < C::CONSUMER_WARPS ? 4 : C::CONSUMER_WARPS;
-    int stage = 0, phase = 0;
-    for (int it = 0;; ++it) {
-        if (it > 0 && lane == 0 && warp == it % R) {   // refill the slot released at it - 1
-            const int sp = stage == 0 ? C::STAGES - 1 : stage - 1;
-            mbar_wait(&empty[sp], (uint32_t)(stage == 0 ? phase ^ 1 : phase));
-            issue_next(sp);
-        }
-        __syncwarp();   // the refilling lane rejoins before the warp-wide mma.sync
-        mbar_wait(&full[stage], (uint32_t)phase);
-        const int4 in = info[stage];
-        if (in.x < 0) break;
-#ifdef DG_TRACE
-        if (it == 0) DG_TRACE_AT(2);
-#endif
-        const uint32_t sA = base + stage * C::STAGE_BYTES;
-        mma_stage<C>(sA, sA + C::A_BYTES, fo, acc);
-        release_slot(&empty[stage], lane);
-        if (++stage == C::STAGES) {
-            stage = 0;
-            phase ^= 1;
-        }
-        if (!in.w) continue;
-        // ---- the unit's last k-step: finish this warp's sub-tile of (tile in.x, slice in.y)
-        int tm, tn;
-        tile_coords(in.x, tiles_m, tiles_n, group_m, tm, tn);
-        bool write = true;
-        if (S > 1) {
-            constexpr int Q = C::E / 4;
-            constexpr int64_t QSTRIDE = (int64_t)C::CONSUMER_WARPS * 32 * 4;
-            double *mine = partial_slot<C>(pk.ws, (int64_t)in.x * S + in.y, warp, lane);
-            const double *flat = &acc[0][0][0][0];
-#pragma unroll
-            for (int q = 0; q < Q; ++q)
-                stg_v4(mine + q * QSTRIDE, flat[4 * q], flat[4 * q + 1], flat[4 * q + 2], flat[4 * q + 3]);
-            __syncwarp();
-            int old = 0;
-            int *ctr = pk.counters + (int64_t)in.x * C::CONSUMER_WARPS + warp;
-            if (lane == 0) {
-                __threadfence();   // the warp's partial (ordered by __syncwarp) before the count
-                old = atomicAdd(ctr, 1);
-            }
-            old = __shfl_sync(0xffffffffu, old, 0);
-            write = (old == S - 1);
-            if (write) {
-                __threadfence();
-                sum_partials<C, 1>(acc, pk.ws, S, [&](int t) { return (int64_t)in.x * S + t; }, warp, lane);
-                if (lane == 0) *ctr = 0;
-            }
-        }
-        if (write)
-            epilogue<C>(acc, tm * C::BM + warp_m * C::WM, tn * C::BN + warp_n * C::WN, lane, M, N, alpha, beta, Cm,
-                        ldc, vec != 0);
-#pragma unroll
-        for (int mb = 0; mb < C::MB; ++mb)
-#pragma unroll
-            for (int np = 0; np < C::NP; ++np)
-#pragma unroll
-                for (int j = 0; j < 2; ++j) acc[mb][np][j][0] = acc[mb][np][j][1] = 0.0;
-    }
-    DG_TRACE_AT(6);
-#ifdef DG_TRACE
-    DG_TRACE_SLOT(7, (unsigned long long)dg_smid());
 #endif
 }
 

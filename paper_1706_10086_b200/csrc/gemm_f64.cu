@@ -527,10 +527,6 @@ int workspace_release_f64() {
 
 static int get_split_ws(cudaStream_t st, size_t doubles, size_t tiles, double **ws, int **ctr);
 
-int split_workspace(cudaStream_t st, size_t doubles, size_t counters, double **ws, int **ctr) {
-    return get_split_ws(st, doubles, counters, ws, ctr);
-}
-
 int streamk_workspace(cudaStream_t st, size_t slot_doubles, int grid, size_t tiles, double **ws, int **ctr) {
     return get_split_ws(st, slot_doubles * 2 * (size_t)grid, tiles, ws, ctr);
 }

@@ -111,35 +111,6 @@ static int launch_streamk(const LaunchArgs &a, cudaStream_t st) {
                       "dgemm_streamk_kernel launch");
 }
 
-// Persistent split-K launch: grid = min(SMs x resident CTAs, units); workspace = the tiles x S
-// partials, (tile, warp) counters and the ticket counter (all self-resetting).
-int split_workspace(cudaStream_t st, size_t doubles, size_t counters, double **ws, int **ctr);
-
-template <class C>
-static int launch_persist(const LaunchArgs &a, cudaStream_t st) {
-    CUtensorMap ta, tb;
-    int rc = make_tmap(&ta, a.A, a.M, a.K, a.lda, C::BM);
-    if (rc) return rc;
-    rc = make_tmap(&tb, a.B, a.K, a.N, a.ldb, 16);
-    if (rc) return rc;
-    const int64_t tiles = ((int64_t)a.M + C::BM - 1) / C::BM * (((int64_t)a.N + C::BN - 1) / C::BN);
-    // every slice must own at least one k-step (the unit stream has no empty units)
-    const int64_t KT = ((int64_t)a.K + C::BK - 1) / C::BK;
-    const int S = (int)std::max<int64_t>(1, std::min<int64_t>(a.sk.splits, KT));
-    const int grid = streamk_grid((const void *)dgemm_persist_kernel<C>, C::CONSUMER_THREADS, C::SMEM_BYTES,
-                                  tiles * S);
-    if (grid <= 0) return set_error(GEMM_ERR_CUDA, "persistent occupancy query failed");
-    if (tiles * S + grid >= 0x7FFFFFFF) return set_error(GEMM_ERR_UNSUPPORTED, "too many work units");
-    PskArgs pk{S, nullptr, nullptr, nullptr};
-    const size_t nctr = (size_t)tiles * C::CONSUMER_WARPS + 1;   // (tile, warp) counters + the ticket counter
-    rc = split_workspace(st, S > 1 ? (size_t)tiles * S * C::BM * C::BN : 1, nctr, &pk.ws, &pk.counters);
-    if (rc) return rc;
-    pk.queue = pk.counters + nctr - 1;
-    return cuda_check(launch_k(dgemm_persist_kernel<C>, dim3(grid), dim3(C::CONSUMER_THREADS), C::SMEM_BYTES, st, ta,
-                               tb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec, a.group_m, pk),
-                      "dgemm_persist_kernel launch");
-}
-
 // Hybrid launch: the W full data-parallel waves as one plain XP launch (grid = W*G tiles),
 // then the tail's k-steps over gsk stream-K CTAs, then the fix-up of the cut tail tiles.
 template <class C>
@@ -211,14 +182,6 @@ static int launch_hybrid(const LaunchArgs &a, cudaStream_t st) {
                            (int)Cfg<BM, BN, BK, WM, WN, ST>::SMEM_BYTES, 1, -3, 0},                           \
              (const void *)dgemm_tma_kernel<Cfg<BM, BN, BK, WM, WN, ST>, 2, false, kRotXP>,                   \
              launch_tma_cluster<Cfg<BM, BN, BK, WM, WN, ST>>}
-
-// persistent split-K: split_k = 0 (slices chosen per call, like *_splitk), one launch
-#define DG_PSK(BM, BN, BK, WM, WN, ST)                                                                    \
-    CfgEntry{"tma_" #BM "x" #BN "x" #BK "_w" #WM "x" #WN "_s" #ST "_persist",                                 \
-             gemm_cfg_desc{BM, BN, BK, WM, WN, ST, Cfg<BM, BN, BK, WM, WN, ST>::CONSUMER_THREADS,              \
-                           (int)Cfg<BM, BN, BK, WM, WN, ST>::SMEM_BYTES, 1, 0, 0},                            \
-             (const void *)dgemm_persist_kernel<Cfg<BM, BN, BK, WM, WN, ST>>,                                 \
-             launch_persist<Cfg<BM, BN, BK, WM, WN, ST>>}
 
 #define DG_TMA_SK(BM, BN, BK, WM, WN, ST, SK, SPLIT, XP, SUFFIX)                                              \
     CfgEntry{"tma_" #BM "x" #BN "x" #BK "_w" #WM "x" #WN "_s" #ST SUFFIX,                                     \

@@ -78,7 +78,7 @@ def test_sass_gemm_kernels_use_dmma_tma_and_no_spills(sass):
             assert "STG.E.ENL2.256" in body, name
             continue
         assert "DMMA.8x8x4" in body, name
-        if "dgemm_tma_kernel" in name or "dgemm_sktail_kernel" in name or "dgemm_persist_kernel" in name:
+        if "dgemm_tma_kernel" in name or "dgemm_sktail_kernel" in name:
             assert "UTMALDG" in body, name
             assert "STG.E.ENL2.256" in body, name
         if "dgemm_generic_kernel" in name:

@@ -683,9 +683,8 @@ def test_hybrid_plan_full_size_tail_rows(cuda_lib, shape):
                                              ("tma_64x64x16_w32x16_s6", None), ("tma_256x64x16_w64x32_s4_xp", None),
                                              ("tma_64x64x16_w32x16_s6_hybrid", None),
                                              ("tma_128x64x16_w32x16_s6_streamk", None),
-                                             ("tma_64x64x32_w32x16_s3_persist", 1), ("tma_64x64x32_w32x16_s3_persist", 4),
                                              ("tma_64x64x32_w32x16_s3_csplit", 4), ("tma_64x64x16_w32x16_s6_csplit", 8),
-                                             ("tma_128x64x32_w32x16_s4_persist", 3)])
+                                             ])
 def test_ring_slot_reuse_exact_k_signature(cuda_lib, cfg_name, splits):
     """Regression for the ring's write-after-read hazard (DESIGN.md §6 "Releasing a slot"):
     with A = ones and B[k][j] = k + 1, every C entry is exactly K(K+1)/2, and a warp that read
@@ -700,55 +699,6 @@ def test_ring_slot_reuse_exact_k_signature(cuda_lib, cfg_name, splits):
         torch.cuda.synchronize()
         bad = int((C != n * (n + 1) / 2).sum())
         assert bad == 0, (cfg_name, splits, bad)
-
-
-# ---------------------------------------------------------------- persistent split-K (row a5)
-def persist_cfgs(G):
-    return [c["id"] for c in G.cfgs() if c["name"].endswith("_persist")]
-
-
-@pytest.mark.parametrize("shape", [(64, 64, 64), (64, 64, 4096), (1024, 1024, 1024), (130, 1000, 96), (2048, 512, 2048),
-                                   (700, 650, 1300)], ids=lambda s: "x".join(map(str, s)))
-def test_persist_exact_regime_bitwise_every_split(cuda_lib, shape):
-    """Persistent split-K: tickets handed out dynamically (which CTA runs which slice varies run
-    to run), per-warp partial publication, the S-th warp to arrive sums the slices in order.
-    Dyadic inputs: every S (1 = persistent data-parallel; S beyond KT leaves empty slices;
-    fewer units than CTAs leaves CTAs with nothing but the end sentinel) gives the exact bits."""
-    M, N, K = shape
-    A, B, C0 = synth.problem(M, N, K, mode="dyadic", seed=M + N)
-    ref = oracle.dgemm(1.5, A, B, 0.5, C0)
-    dA, dB = dev(A), dev(B)
-    for cfg in persist_cfgs(cuda_lib):
-        for S in (1, 2, 3, 4, 8, 16):
-            dC = dev(C0)
-            cuda_lib.gemm(dA, dB, dC, 1.5, 0.5, cfg=cfg, splits=S)
-            torch.cuda.synchronize()
-            assert np.array_equal(dC.cpu().numpy(), ref), (cuda_lib.cfg_name(cfg), S)
-
-
-def test_persist_uniform_within_bound_deterministic_and_counters_reset(cuda_lib):
-    """Uniform inputs: within the bound, bitwise repeatable over 30 back-to-back launches on one
-    stream with the split count and the shape changing in between (the ticket counter and the
-    (tile, warp) counters reset themselves), and S = 1 equals the plain one-pass kernels."""
-    A, B, C0 = synth.problem(520, 776, 1000, seed=44)
-    A2, B2, C2 = synth.problem(64, 192, 256, seed=45)
-    dA, dB, dA2, dB2 = dev(A), dev(B), dev(A2), dev(B2)
-    for cfg in persist_cfgs(cuda_lib):
-        first = {}
-        for it in range(30):
-            S = (1, 4, 5)[it % 3]
-            dC = dev(C0)
-            cuda_lib.gemm(dA, dB, dC, 1.5, 0.5, cfg=cfg, splits=S)
-            if it % 4 == 0:   # an unrelated launch in between
-                cuda_lib.gemm(dA2, dB2, dev(C2), 1.0, 0.0, cfg=cfg, splits=2)
-            torch.cuda.synchronize()
-            out = dC.cpu().numpy()
-            if S not in first:
-                first[S] = out
-                check_vs_oracle(out, A, B, C0, 1.5, 0.5)
-            assert np.array_equal(out, first[S]), (cuda_lib.cfg_name(cfg), it, S)
-        plain = run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=cuda_lib.cfg_id("tma_64x64x32_w16x32_s3"))
-        assert np.array_equal(first[1], plain), cuda_lib.cfg_name(cfg)
 
 
 # ---------------------------------------------------------------- cluster split-K (row a5)
