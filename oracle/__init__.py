@@ -39,11 +39,15 @@ U = 2.0 ** -53
 
 
 def build(force: bool = False) -> str:
-    """Compile the oracle with gcc: -O2, no FMA contraction, no fast-math."""
+    """Compile the oracle with gcc: -O2, no FMA contraction, no fast-math.  The library is
+    written to a per-process temporary name and renamed into place, so ranks of a multi-GPU
+    run that build concurrently never load a half-written file."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = f"{_LIB}.{os.getpid()}.tmp"
         cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
-               "-pthread", "-o", _LIB, _SRC, "-lm"]
+               "-pthread", "-o", tmp, _SRC, "-lm"]
         subprocess.check_call(cmd)
+        os.replace(tmp, _LIB)
     return _LIB
 
 
