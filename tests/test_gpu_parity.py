@@ -454,6 +454,62 @@ def test_config5_one_rank_shard_sampled(cuda_lib):
     torch.cuda.empty_cache()
 
 
+def _sampled_rows_check(G, dA, dB, dC, M, N, K, rows, c0, nc, seed, alpha, beta, mode="uniform"):
+    B = synth.matrix(mode, seed, 1, K, N, col0=c0, ncols=nc)
+    A_r = np.vstack([synth.matrix(mode, seed, 0, M, K, row0=r, nrows=1) for r in rows])
+    C0 = np.vstack([synth.matrix(mode, seed, 2, M, N, row0=r, nrows=1, col0=c0, ncols=nc) for r in rows])
+    ref, mag = oracle.dgemm(alpha, A_r, B, beta, C0, want_mag=True)
+    got = dC[torch.tensor(rows, device="cuda")][:, c0:c0 + nc].cpu().numpy()
+    res = oracle.check(got, ref, oracle.bound(K, alpha, beta, mag, C0))
+    assert res.ok, str(res)
+    return res
+
+
+def test_max_size_c_beyond_2_31_elements(cuda_lib):
+    """Element offsets past 2^31: C is 65600 x 32800 (2.15e9 entries, 17 GB), ragged in both
+    tile dimensions, so rows near the end address C at 64-bit offsets in the epilogue; the
+    plan's own kernel, alpha = 1.5, beta = 0.5, last rows and a ragged right-edge block checked
+    against the oracle."""
+    M, N, K, seed = 65600, 32800, 40, 61
+    assert M * N > 2 ** 31
+    dA = torch.empty((M, K), dtype=torch.float64, device="cuda")
+    dB = torch.empty((K, N), dtype=torch.float64, device="cuda")
+    dC = torch.empty((M, N), dtype=torch.float64, device="cuda")
+    for X, mat in ((dA, 0), (dB, 1), (dC, 2)):
+        cuda_lib.fill(X, "uniform", seed, mat)
+    cuda_lib.gemm(dA, dB, dC, 1.5, 0.5)
+    torch.cuda.synchronize()
+    rows = [0, 32767, 32768, 65535, 65536, 65599]
+    _sampled_rows_check(cuda_lib, dA, dB, dC, M, N, K, rows, N - 300, 300, seed, 1.5, 0.5)
+    _sampled_rows_check(cuda_lib, dA, dB, dC, M, N, K, rows, 0, 256, seed, 1.5, 0.5)
+    del dA, dB, dC
+    torch.cuda.empty_cache()
+
+
+def test_max_size_k_beyond_2_20(cuda_lib):
+    """Long K: 136 x 200 x (2^20 + 24) (tens of thousands of k-steps per tile, ragged K tail),
+    with the product's plan and with split-K and cluster split-K forced, sampled rows against
+    the oracle; and an all-ones problem of the same K must give K exactly in every entry."""
+    M, N, K, seed = 136, 200, 2 ** 20 + 24, 62
+    dA = torch.empty((M, K), dtype=torch.float64, device="cuda")
+    dB = torch.empty((K, N), dtype=torch.float64, device="cuda")
+    dC = torch.empty((M, N), dtype=torch.float64, device="cuda")
+    for cfg, S in ((None, None), (cuda_lib.cfg_id("tma_64x64x32_w32x16_s3_splitk"), 16),
+                   (cuda_lib.cfg_id("tma_64x64x32_w32x16_s3_csplit"), 8)):
+        for X, mat in ((dA, 0), (dB, 1), (dC, 2)):
+            cuda_lib.fill(X, "uniform", seed, mat)
+        cuda_lib.gemm(dA, dB, dC, 1.5, 0.5, cfg=cfg, splits=S)
+        torch.cuda.synchronize()
+        _sampled_rows_check(cuda_lib, dA, dB, dC, M, N, K, [0, 67, 135], 0, N, seed, 1.5, 0.5)
+    dA.fill_(1.0)
+    dB.fill_(1.0)
+    cuda_lib.gemm(dA, dB, dC, 1.0, 0.0)
+    torch.cuda.synchronize()
+    assert bool((dC == float(K)).all())
+    del dA, dB, dC
+    torch.cuda.empty_cache()
+
+
 # ---------------------------------------------------------------- host entry point (e2e)
 def test_host_entry_point(cuda_lib):
     A, B, C0 = synth.problem(700, 650, 300, seed=4)
