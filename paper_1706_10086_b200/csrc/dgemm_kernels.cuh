@@ -347,12 +347,65 @@ __device__ __forceinline__ bool partial_reduce(double (&acc)[C::MB][C::NP][2][2]
     return true;
 }
 
-// returns true if this CTA must run the epilogue (no split, or last split to arrive)
+// Split-K finish, ordered by slice (returns true if this CTA runs the epilogue: no split, or the
+// last slice).  Slices 0..S-2 store their raw partial, and thread 0 publishes it with one
+// red.release on the tile's counter after a CTA barrier (the barrier orders every thread's
+// stores before the release) -- then the CTA exits without waiting for anything.  Slice S-1
+// keeps its own partial, waits (ld.acquire) until the counter reaches S-1, and adds
+// partials 0..S-2 and then its own, i.e. (((0 + p0) + p1) + ...) + p_{S-1}: the order, hence
+// the bits, of summing all S partials in slice order.  The last slice's wait relies on the
+// block scheduler dispatching CTAs in linear order (slices 0..S-2 of a tile have lower
+// linear indices than slice S-1, gridDim.y = S), as serial split-K schemes do; the previous
+// scheme (every slice stores, the last to arrive on an atomic sums) made each CTA wait for
+// its atomic's round trip and the reducer re-read its own partial (per-CTA traces).
 template <class C>
 __device__ __forceinline__ bool split_reduce(double (&acc)[C::MB][C::NP][2][2], const SplitArgs &sk, int tile,
-                                             int s, int warp, int lane) {
-    if (sk.splits <= 1) return true;
-    return partial_reduce<C>(acc, sk.ws, sk.counters, tile, sk.splits, s, sk.splits, warp, lane);
+                                             int s, int warp, int lane, uint32_t smem_base) {
+    const int S = sk.splits;
+    if (S <= 1) return true;
+    if constexpr (C::E >= 32) {   // large warp tiles: the last-arriver scheme (no registers to spare)
+        return partial_reduce<C>(acc, sk.ws, sk.counters, tile, S, s, S, warp, lane);
+    }
+    constexpr int Q = C::E / 4;
+    constexpr int64_t QSTRIDE = (int64_t)C::CONSUMER_WARPS * 32 * 4;
+    int *ctr = sk.counters + tile;
+    double *flat = &acc[0][0][0][0];
+    if (s < S - 1) {
+        double *mine = partial_slot<C>(sk.ws, (int64_t)tile * S + s, warp, lane);
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+            stg_v4(mine + q * QSTRIDE, flat[4 * q], flat[4 * q + 1], flat[4 * q + 2], flat[4 * q + 3]);
+        __syncthreads();
+        if (threadIdx.x == 0) red_release_add(ctr, 1);
+        return false;
+    }
+    // the last slice: park the own partial in the drained ring, wait for the others
+    static_assert(C::STAGES * C::STAGE_BYTES >= (uint32_t)C::E * C::CONSUMER_THREADS * 8, "own partial fits");
+    __syncthreads();   // every warp is done with the ring
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const uint32_t a = smem_base + (uint32_t)(((q * C::CONSUMER_WARPS + warp) * 32 + lane) * 32);
+        sts_v2(a, flat[4 * q], flat[4 * q + 1]);
+        sts_v2(a + 16, flat[4 * q + 2], flat[4 * q + 3]);
+    }
+    if (threadIdx.x == 0)
+        while (ld_acquire(ctr) < S - 1) {
+        }
+    __syncthreads();   // thread 0's acquire orders the others' partials before every thread's loads
+    sum_partials<C>(acc, sk.ws, S - 1, [&](int t) { return (int64_t)tile * S + t; }, warp, lane);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const uint32_t a = smem_base + (uint32_t)(((q * C::CONSUMER_WARPS + warp) * 32 + lane) * 32);
+        double v0, v1, v2, v3;
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v0), "=d"(v1) : "r"(a));
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v2), "=d"(v3) : "r"(a + 16));
+        flat[4 * q] += v0;
+        flat[4 * q + 1] += v1;
+        flat[4 * q + 2] += v2;
+        flat[4 * q + 3] += v3;
+    }
+    if (threadIdx.x == 0) *ctr = 0;   // ready for the next launch on this stream
+    return true;
 }
 
 // Cluster split-K (SPLIT == 2, row a5): the S = gridDim.y slices of a tile run as one thread-
@@ -542,7 +595,7 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
             return;
         }
     } else if constexpr (SPLIT == 1) {
-        if (!split_reduce<C>(acc, sk, blockIdx.x, split, warp, lane)) {
+        if (!split_reduce<C>(acc, sk, blockIdx.x, split, warp, lane, base)) {
             DG_TRACE_AT(6);
             return;
         }

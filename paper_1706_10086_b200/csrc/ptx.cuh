@@ -107,6 +107,16 @@ __device__ __forceinline__ void sts_v2(uint32_t addr, double x, double y) {
     asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(addr), "d"(x), "d"(y) : "memory");
 }
 
+// ---- gpu-scope release / acquire on a global counter (ordered split-K) -----------------------
+__device__ __forceinline__ void red_release_add(int *p, int v) {
+    asm volatile("red.release.gpu.global.add.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire(const int *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 // ---- programmatic dependent launch (PDL) -------------------------------------------
 // The host launches every GEMM kernel with programmatic stream serialization, so a kernel
 // may become resident while the previous kernel in the stream is still draining.  Each

@@ -1,0 +1,9 @@
+set -x
+timeout -s KILL 120 python tools/cfg_time.py plan,tma_64x64x32_w32x16_s3_splitk:2,tma_64x64x32_w32x16_s3_splitk:4 512,1024 > gpurun_out/r02_ordered_quick.jsonl 2> gpurun_out/r02_ordered_quick.err
+echo quick rc=$?
+cat gpurun_out/r02_ordered_quick.jsonl | cut -c1-150
+timeout -s KILL 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "split or cluster or ring_slot or small_sizes or max_size or graph" > gpurun_out/r02_ordered_tests.txt 2>&1
+echo tests rc=$?
+tail -3 gpurun_out/r02_ordered_tests.txt
+timeout -s KILL 300 python tools/cfg_time.py plan,tma_64x64x32_w32x16_s3_splitk:2,tma_64x64x32_w32x16_s3_splitk:3,tma_64x64x32_w32x16_s3_splitk:4,tma_64x64x32_w32x16_s3_splitk:6,tma_64x64x16_w32x16_s6_splitk:4,tma_64x64x16_w32x16_s6_splitk:8 256,384,512,640,768,1024,1536,2048,1024x1024x4096,1024x1024x65536 > gpurun_out/r02_ordered_cfgs.jsonl 2> gpurun_out/r02_ordered_cfgs.err
+timeout -s KILL 120 python tools/trace_ctas.py tma_64x64x32_w32x16_s3_splitk:4,tma_64x64x32_w32x16_s3_splitk:2 1024x1024x1024,512x512x512 > gpurun_out/r02_trace_ordered.jsonl 2> gpurun_out/r02_trace_ordered.err
