@@ -454,7 +454,7 @@ def test_config5_one_rank_shard_sampled(cuda_lib):
     torch.cuda.empty_cache()
 
 
-def _sampled_rows_check(G, dA, dB, dC, M, N, K, rows, c0, nc, seed, alpha, beta, mode="uniform"):
+def _rows_block_vs_oracle(G, dA, dB, dC, M, N, K, rows, c0, nc, seed, alpha, beta, mode="uniform"):
     B = synth.matrix(mode, seed, 1, K, N, col0=c0, ncols=nc)
     A_r = np.vstack([synth.matrix(mode, seed, 0, M, K, row0=r, nrows=1) for r in rows])
     C0 = np.vstack([synth.matrix(mode, seed, 2, M, N, row0=r, nrows=1, col0=c0, ncols=nc) for r in rows])
@@ -480,8 +480,8 @@ def test_max_size_c_beyond_2_31_elements(cuda_lib):
     cuda_lib.gemm(dA, dB, dC, 1.5, 0.5)
     torch.cuda.synchronize()
     rows = [0, 32767, 32768, 65535, 65536, 65599]
-    _sampled_rows_check(cuda_lib, dA, dB, dC, M, N, K, rows, N - 300, 300, seed, 1.5, 0.5)
-    _sampled_rows_check(cuda_lib, dA, dB, dC, M, N, K, rows, 0, 256, seed, 1.5, 0.5)
+    _rows_block_vs_oracle(cuda_lib, dA, dB, dC, M, N, K, rows, N - 300, 300, seed, 1.5, 0.5)
+    _rows_block_vs_oracle(cuda_lib, dA, dB, dC, M, N, K, rows, 0, 256, seed, 1.5, 0.5)
     del dA, dB, dC
     torch.cuda.empty_cache()
 
@@ -500,7 +500,7 @@ def test_max_size_k_beyond_2_20(cuda_lib):
             cuda_lib.fill(X, "uniform", seed, mat)
         cuda_lib.gemm(dA, dB, dC, 1.5, 0.5, cfg=cfg, splits=S)
         torch.cuda.synchronize()
-        _sampled_rows_check(cuda_lib, dA, dB, dC, M, N, K, [0, 67, 135], 0, N, seed, 1.5, 0.5)
+        _rows_block_vs_oracle(cuda_lib, dA, dB, dC, M, N, K, [0, 67, 135], 0, N, seed, 1.5, 0.5)
     dA.fill_(1.0)
     dB.fill_(1.0)
     cuda_lib.gemm(dA, dB, dC, 1.0, 0.0)
