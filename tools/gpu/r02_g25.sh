@@ -1,0 +1,6 @@
+set -x
+timeout -s KILL 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_freivalds.py -m gpu -x -q -k "split or cluster or ring_slot or small_sizes or max_size or graph or config2 or hybrid" > gpurun_out/r02_interleave_tests.txt 2>&1
+echo tests rc=$?
+tail -2 gpurun_out/r02_interleave_tests.txt
+timeout -s KILL 300 python tools/cfg_time.py plan,tma_64x64x32_w32x16_s3_splitk:2,tma_64x64x32_w32x16_s3_splitk:3,tma_64x64x32_w32x16_s3_splitk:4,tma_64x64x32_w32x16_s3_splitk:6,tma_64x64x16_w32x16_s6_splitk:4 256,384,512,640,768,1024,1536,2048,1024x1024x4096,1024x1024x65536 > gpurun_out/r02_interleave_cfgs.jsonl 2> gpurun_out/r02_interleave_cfgs.err
+timeout -s KILL 120 python tools/trace_ctas.py tma_64x64x32_w32x16_s3_splitk:4,tma_64x64x32_w32x16_s3_splitk:2 1024x1024x1024,512x512x512 > gpurun_out/r02_trace_interleave.jsonl 2> gpurun_out/r02_trace_interleave.err
