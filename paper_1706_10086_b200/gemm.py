@@ -154,34 +154,46 @@ def _mat(x, name, dtype="float64"):
 
 
 _RAW_STREAM = None
+_CUR_DEV = None
 
 
-def _current_raw_stream():
-    """cudaStream_t of torch's current stream on the current device.  torch's raw-pointer
-    query (what Triton's launcher uses) costs ~0.3 us against ~3 us for building a
-    torch.cuda.Stream object, a large share of a small GEMM's host cost; the public API is
-    the fallback if the private one is absent."""
+def _current_device() -> int:
+    """torch's current CUDA device index: the C-level query (~0.1 us) rather than
+    torch.cuda.current_device() (~1 us, it re-checks lazy initialisation), falling back to
+    the public API if the private one is absent."""
+    global _CUR_DEV
+    if _CUR_DEV is None:
+        import torch
+        fast = getattr(torch._C, "_cuda_getDevice", None)
+        _CUR_DEV = fast if fast is not None else torch.cuda.current_device
+    return _CUR_DEV()
+
+
+def _current_raw_stream(dev=None):
+    """cudaStream_t of torch's current stream on device `dev` (default: the current one).
+    torch's raw-pointer query (what Triton's launcher uses) costs ~0.3 us against ~3 us for
+    building a torch.cuda.Stream object, a large share of a small GEMM's host cost; the
+    public API is the fallback if the private one is absent."""
     global _RAW_STREAM
     import torch
     if _RAW_STREAM is None:
         raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
-        _RAW_STREAM = (lambda: raw(torch.cuda.current_device())) if raw is not None else \
-            (lambda: torch.cuda.current_stream().cuda_stream)
-    return _RAW_STREAM()
+        _RAW_STREAM = raw if raw is not None else (lambda d: torch.cuda.current_stream(d).cuda_stream)
+    return _RAW_STREAM(_current_device() if dev is None else dev)
 
 
-def _stream_ptr(stream):
+def _stream_ptr(stream, dev=None):
     if stream is None:
-        return _current_raw_stream()
+        return _current_raw_stream(dev)
     if isinstance(stream, int):
         return stream
     return stream.cuda_stream
 
 
 def _on_current_device(*ts, names="ABC"):
-    """Every tensor is a CUDA tensor on the current device (the library launches there)."""
-    import torch
-    dev = torch.cuda.current_device()
+    """Every tensor is a CUDA tensor on the current device (the library launches there).
+    Returns the device index."""
+    dev = _current_device()
     for t, n in zip(ts, names):
         d = t.get_device()   # -1 for CPU tensors
         if d != dev:
@@ -189,6 +201,7 @@ def _on_current_device(*ts, names="ABC"):
                 raise ValueError(f"{n} must be a CUDA tensor (use gemm_host for host buffers)")
             raise ValueError(f"{n} is on cuda:{d} but the current device is cuda:{dev} "
                              "(torch.cuda.set_device or move the tensor)")
+    return dev
 
 
 def gemm(A, B, C, alpha: float = 1.0, beta: float = 0.0, cfg: int | None = None, stream=None,
@@ -199,8 +212,7 @@ def gemm(A, B, C, alpha: float = 1.0, beta: float = 0.0, cfg: int | None = None,
     pc, M2, N2, ldc = _mat(C, "C")
     if K2 != K or M2 != M or N2 != N:
         raise ValueError(f"shape mismatch A{tuple(A.shape)} B{tuple(B.shape)} C{tuple(C.shape)}")
-    _on_current_device(A, B, C)
-    st = _stream_ptr(stream)
+    st = _stream_ptr(stream, _on_current_device(A, B, C))
     if cfg is None and splits is None:
         rc = _lib.gemm_f64_stream(M, N, K, float(alpha), pa, lda, pb, ldb, float(beta), pc, ldc, st)
     elif splits is None:
