@@ -389,8 +389,7 @@ __device__ __forceinline__ bool split_reduce(double (&acc)[C::MB][C::NP][2][2], 
         sts_v2(a + 16, flat[4 * q + 2], flat[4 * q + 3]);
     }
     if (threadIdx.x == 0)
-        while (ld_acquire(ctr) < S - 1) {
-        }
+        while (ld_acquire(ctr) < S - 1) __nanosleep(32);   // rarely taken: the siblings were dispatched first
     __syncthreads();   // thread 0's acquire orders the others' partials before every thread's loads
     sum_partials<C>(acc, sk.ws, S - 1, [&](int t) { return (int64_t)tile * S + t; }, warp, lane);
 #pragma unroll
