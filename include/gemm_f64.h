@@ -182,9 +182,10 @@ GEMM_API int gemm_cfg_select(int64_t M, int64_t N, int64_t K, const double *A, i
                     const double *B, int64_t ldb);
 
 /* The full launch plan of the heuristic: configuration id and number of
- * deterministic split-K slices (1 = no split; >1 only for *_splitk configurations:
- * each slice multiplies a contiguous k-range into a workspace partial and the
- * last slice to finish sums the partials in slice order, row a5). */
+ * deterministic split-K slices (1 = no split; >1 only for *_splitk / *_csplit configurations:
+ * each slice multiplies a contiguous k-range; slices 0..S-2 publish a workspace partial and the
+ * last slice adds them and its own in slice order (*_csplit: through distributed shared memory
+ * of the slices' cluster), row a5). */
 GEMM_API int gemm_plan(int64_t M, int64_t N, int64_t K, const double *A, int64_t lda,
               const double *B, int64_t ldb, int *cfg_id, int *splits);
 
