@@ -220,6 +220,15 @@ __device__ __forceinline__ void epilogue(const double (&acc)[C::MB][C::NP][2][2]
     }
 }
 
+// floor(a * b / c) for 0 <= a, b and 0 < c: a 32-bit division when the product fits (always,
+// for k-step ranges), the 64-bit one only otherwise (a long software sequence; the per-CTA
+// trace put the prologue at 0.65 us)
+__device__ __forceinline__ int mul_div(int a, int b, int c) {
+    const unsigned long long p = (unsigned long long)(unsigned)a * (unsigned)b;
+    if (p <= 0xffffffffull) return (int)((unsigned)p / (unsigned)c);
+    return (int)(p / (unsigned long long)c);
+}
+
 // Grouped raster (row a1): consecutive CTAs walk group_m tile-rows column by column.
 __device__ __forceinline__ void tile_coords(int bid, int tiles_m, int tiles_n, int group_m, int &tm, int &tn) {
     const int per_group = group_m * tiles_n;
@@ -240,10 +249,21 @@ __device__ __forceinline__ void tile_coords(int bid, int tiles_m, int tiles_n, i
 // expect_tx).  STAGES-1 stages stay in flight ahead of the slowest warp.
 template <class C>
 __device__ __forceinline__ void tma_issue_stage(uint8_t *stage_ptr, const CUtensorMap *tmA, const CUtensorMap *tmB,
-                                                uint64_t *full_bar, int m0, int n0, int kt, uint64_t pol) {
+                                                uint64_t *full_bar, int m0, int n0, int kt, uint64_t pol,
+                                                bool md = false) {
     mbar_arrive_expect_tx(full_bar, C::STAGE_BYTES);
     uint8_t *sA = stage_ptr;
     uint8_t *sB = stage_ptr + C::A_BYTES;
+    if (md) {
+        // multi-dimensional maps (K % 16 == 0, N % 16 == 0; host: make_tmap_a3 / make_tmap_b4):
+        // A as (16 columns, rows, k-groups), box (16, BM, KG) -> smem [kg][row][16];
+        // B as (16 columns, 16 rows, 16-column panels, k-groups), box (16, 16, BN/16, KG) ->
+        // smem [kg][panel][row][16] -- the same swizzled layout the 2-D boxes fill, in 2
+        // instructions per stage instead of KG * (1 + BN/16)
+        tma_load_3d(sA, tmA, 0, m0, kt * C::KG, full_bar, pol);
+        tma_load_4d(sB, tmB, 0, 0, n0 / 16, kt * C::KG, full_bar, pol);
+        return;
+    }
 #pragma unroll
     for (int kg = 0; kg < C::KG; ++kg) {
         const int k = kt * C::BK + kg * 16;
@@ -483,9 +503,10 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
     const int KT = (K + C::BK - 1) / C::BK;
     const int split = SPLIT ? (int)blockIdx.y : 0;
     const int nsplit = SPLIT == 2 ? (int)gridDim.y : (SPLIT ? sk.splits : 1);
-    const int kt0 = (int)(((int64_t)split * KT) / nsplit);
-    const int NK = (int)(((int64_t)(split + 1) * KT) / nsplit) - kt0;   // k-steps of this CTA
+    const int kt0 = mul_div(split, KT, nsplit);
+    const int NK = mul_div(split + 1, KT, nsplit) - kt0;   // k-steps of this CTA
     const bool producer = (threadIdx.x == 0);
+    const bool md = (vec & 2) != 0;   // stage A / B with the 3-D / 4-D tensor maps
     constexpr int R = ROT < C::CONSUMER_WARPS ? ROT : C::CONSUMER_WARPS;   // warps sharing the refills
     uint64_t pol = 0;
 
@@ -504,8 +525,12 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
     DG_TRACE_AT(1);
     griddep_launch();
     if (producer) {
-        for (int s = 0; s < C::STAGES && s < NK; ++s)
-            tma_issue_stage<C>(base_ptr + s * C::STAGE_BYTES, &tmA, &tmB, &full[s], m0, n0, kt0 + s, pol);
+        for (int s = 0; s < C::STAGES && s < NK; ++s) {
+            tma_issue_stage<C>(base_ptr + s * C::STAGE_BYTES, &tmA, &tmB, &full[s], m0, n0, kt0 + s, pol, md);
+#ifdef DG_TRACE
+            if (s == 0) DG_TRACE_AT(5);   // the first stage's TMA issued
+#endif
+        }
     }
     __syncthreads();
 
@@ -529,7 +554,7 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
                     const int sp = (i - 1) % C::STAGES;
                     mbar_wait(&empty[sp], ((i - 1) / C::STAGES) & 1);
                     tma_issue_stage<C>(base_ptr + sp * C::STAGE_BYTES, &tmA, &tmB, &full[sp], m0, n0, kt0 + in,
-                                       pol);
+                                       pol, md);
                 }
             }
             if (R > 1) __syncwarp();   // the refilling lane rejoins before the warp-wide mma.sync
@@ -557,7 +582,7 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
                     const int sp = (i - 1) % C::STAGES;
                     mbar_wait(&empty[sp], ((i - 1) / C::STAGES) & 1);
                     tma_issue_stage<C>(base_ptr + sp * C::STAGE_BYTES, &tmA, &tmB, &full[sp], m0, n0, kt0 + in,
-                                       pol);
+                                       pol, md);
                 }
             }
             if (R > 1) __syncwarp();   // the refilling lane rejoins before the warp-wide mma.sync
@@ -589,7 +614,7 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
     if constexpr (SPLIT == 2) {
         if (gridDim.y > 1) {
             cluster_reduce_epilogue<C>(acc, base, warp, lane, m0 + warp_m * C::WM + (lane >> 2),
-                                       n0 + warp_n * C::WN + 4 * (lane & 3), M, N, alpha, beta, Cm, ldc, vec != 0);
+                                       n0 + warp_n * C::WN + 4 * (lane & 3), M, N, alpha, beta, Cm, ldc, (vec & 1) != 0);
             DG_TRACE_AT(6);
             return;
         }
@@ -600,7 +625,7 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
         }
     }
     DG_TRACE_AT(4);
-    epilogue<C>(acc, m0 + warp_m * C::WM, n0 + warp_n * C::WN, lane, M, N, alpha, beta, Cm, ldc, vec != 0);
+    epilogue<C>(acc, m0 + warp_m * C::WM, n0 + warp_n * C::WN, lane, M, N, alpha, beta, Cm, ldc, (vec & 1) != 0);
     DG_TRACE_AT(6);
 #ifdef DG_TRACE
     DG_TRACE_SLOT(7, (unsigned long long)dg_smid() | (1ull << 32));
@@ -680,7 +705,7 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
         int tm, tn;
         tile_coords(t, tiles_m, tiles_n, group_m, tm, tn);
         tma_issue_stage<C>(base_ptr + slot * C::STAGE_BYTES, &tmA, &tmB, &full[slot], tm * C::BM, tn * C::BN,
-                           u - t * KT, pol);
+                           u - t * KT, pol, (vec & 2) != 0);
     };
     const int nloc = u1 - u0;   // k-steps of this CTA
 
@@ -757,7 +782,7 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
         }
         if (do_epi)
             epilogue<C>(acc, tm * C::BM + warp_m * C::WM, tn * C::BN + warp_n * C::WN, lane, M, N, alpha, beta, Cm,
-                        ldc, vec != 0);
+                        ldc, (vec & 1) != 0);
 #ifdef DG_TRACE
         if (t0 + kb == u0) DG_TRACE_AT(4);
 #endif
@@ -822,7 +847,7 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
         int tm, tn;
         tile_coords(hy.tile0 + t, tiles_m, tiles_n, group_m, tm, tn);
         tma_issue_stage<C>(base_ptr + slot * C::STAGE_BYTES, &tmA, &tmB, &full[slot], tm * C::BM, tn * C::BN,
-                           u - t * KT, pol);
+                           u - t * KT, pol, (vec & 2) != 0);
     };
 
     if (producer) {
@@ -903,7 +928,7 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
             int tm, tn;
             tile_coords(hy.tile0 + t, tiles_m, tiles_n, group_m, tm, tn);
             epilogue<C>(acc, tm * C::BM + warp_m * C::WM, tn * C::BN + warp_n * C::WN, lane, M, N, alpha, beta, Cm,
-                        ldc, vec != 0);
+                        ldc, (vec & 1) != 0);
         } else {
             constexpr int Q = C::E / 4;
             constexpr int64_t QSTRIDE = (int64_t)C::CONSUMER_WARPS * 32 * 4;
@@ -967,7 +992,7 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, 1)
         const int q = qb + u;
         const int mb = q / C::NP, np = q - mb * C::NP;
         const double w[4] = {x[u][0], x[u][2], x[u][1], x[u][3]};   // (j,i) = (0,0), (1,0), (0,1), (1,1)
-        epilogue_quad(w, row0 + mb * 8, col0 + np * 16, M, N, alpha, beta, Cm, ldc, vec != 0);
+        epilogue_quad(w, row0 + mb * 8, col0 + np * 16, M, N, alpha, beta, Cm, ldc, (vec & 1) != 0);
     }
 }
 
@@ -1050,7 +1075,7 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, 1)
         mma_stage<C>(sA, sA + C::A_BYTES, fo, acc);
     }
     cp_async_wait<0>();
-    epilogue<C>(acc, m0 + warp_m * C::WM, n0 + warp_n * C::WN, lane, M, N, alpha, beta, Cm, ldc, vec != 0);
+    epilogue<C>(acc, m0 + warp_m * C::WM, n0 + warp_n * C::WN, lane, M, N, alpha, beta, Cm, ldc, (vec & 1) != 0);
 }
 
 }  // namespace dg

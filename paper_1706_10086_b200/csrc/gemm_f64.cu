@@ -144,6 +144,76 @@ int make_tmap_f32(CUtensorMap *map, const float *ptr, int64_t rows, int64_t cols
     return GEMM_OK;
 }
 
+// Multi-dimensional views for one-instruction stages (dgemm_kernels.cuh tma_issue_stage):
+//  A (rows x K, ld): dims (16 columns, rows, K/16 k-groups), strides (ld*8, 128 B), box (16, BM, KG)
+//  B (K x N, ld):    dims (16 columns, 16 rows, N/16 panels, K/16 k-groups),
+//                    strides (ld*8, 128 B, 16*ld*8), box (16, 16, BN/16, KG)
+// Valid only when K % 16 == 0 (A) and K, N % 16 == 0 (B): then every element a box reads is
+// inside the matrix or zero-filled out of range exactly as the 2-D boxes.  Cached like make_tmap.
+static int encode_tmap_md(CUtensorMap *map, const double *ptr, int rank, const cuuint64_t *dims,
+                          const cuuint64_t *strides, const cuuint32_t *box) {
+    auto fn = encode_fn();
+    if (!fn) return set_error(GEMM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+    cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)rank, const_cast<double *>(ptr), dims, strides,
+                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_error(GEMM_ERR_CUDA, "cuTensorMapEncodeTiled (%d-D) failed (%d)", rank, (int)r);
+    return GEMM_OK;
+}
+
+static TmapSlot g_tmap_md_cache[kTmapSlots];
+
+static int make_tmap_md(CUtensorMap *map, const double *ptr, int64_t rows, int64_t cols, int64_t ld, int box,
+                        int kg, bool is_b) {
+    // key: box_rows field carries (is_b, box, kg)
+    const TmapKey key{ptr, rows, cols, ld, (is_b ? 1 << 30 : 0) | (box << 8) | kg};
+    const uint64_t h = ((uint64_t)(uintptr_t)ptr * 0x9E3779B97F4A7C15ull) ^ ((uint64_t)rows * 0xC2B2AE3D27D4EB4Full) ^
+                       ((uint64_t)cols * 0x165667B19E3779F9ull) ^ ((uint64_t)ld << 7) ^ (uint64_t)key.box_rows;
+    TmapSlot &slot = g_tmap_md_cache[(h >> 32) % kTmapSlots];
+    {
+        std::lock_guard<std::mutex> lk(g_tmap_mu);
+        if (slot.valid && slot.key == key) {
+            *map = slot.map;
+            return GEMM_OK;
+        }
+    }
+    int rc;
+    if (!is_b) {   // A: rows x cols(K)
+        const cuuint64_t dims[3] = {16, (cuuint64_t)rows, (cuuint64_t)(cols / 16)};
+        const cuuint64_t strides[2] = {(cuuint64_t)(ld * 8), 128};
+        const cuuint32_t bx[3] = {16, (cuuint32_t)box, (cuuint32_t)kg};
+        rc = encode_tmap_md(map, ptr, 3, dims, strides, bx);
+    } else {       // B: rows(K) x cols(N)
+        const cuuint64_t dims[4] = {16, 16, (cuuint64_t)(cols / 16), (cuuint64_t)(rows / 16)};
+        const cuuint64_t strides[3] = {(cuuint64_t)(ld * 8), 128, (cuuint64_t)(16 * ld * 8)};
+        const cuuint32_t bx[4] = {16, 16, (cuuint32_t)(box / 16), (cuuint32_t)kg};
+        rc = encode_tmap_md(map, ptr, 4, dims, strides, bx);
+    }
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(g_tmap_mu);
+    slot.valid = true;
+    slot.key = key;
+    slot.map = *map;
+    return GEMM_OK;
+}
+
+// Both multi-dimensional maps of a launch, or GEMM_ERR_UNSUPPORTED (then the 2-D boxes are used).
+// GEMM_TMA_MD=0 in the environment disables them (A/B measurements).
+int make_tmaps_md(CUtensorMap *ta, CUtensorMap *tb, const double *A, int64_t M, int64_t K, int64_t lda,
+                  const double *B, int64_t N, int64_t ldb, int bm, int bn, int kg) {
+    static const bool on = [] {
+        const char *e = std::getenv("GEMM_TMA_MD");
+        return !(e && e[0] == '0');
+    }();
+    if (!on || K % 16 || N % 16 || K < 16 || N < 16 || bn % 16) return GEMM_ERR_UNSUPPORTED;
+    if (make_tmap_md(ta, A, M, K, lda, bm, kg, false) || make_tmap_md(tb, B, K, N, ldb, bn, kg, true)) {
+        clear_error();
+        return GEMM_ERR_UNSUPPORTED;
+    }
+    return GEMM_OK;
+}
+
 static int encode_tmap(CUtensorMap *map, const double *ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
     auto fn = encode_fn();
     if (!fn) return set_error(GEMM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");

@@ -14,6 +14,9 @@
 namespace dg {
 
 int make_tmap(CUtensorMap *map, const double *ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows);
+int make_tmaps_md(CUtensorMap *ta, CUtensorMap *tb, const double *A, int64_t M, int64_t K, int64_t lda,
+                  const double *B, int64_t N, int64_t ldb, int bm, int bn, int kg);
+
 
 struct LaunchArgs {
     int M, N, K;
@@ -29,6 +32,20 @@ struct LaunchArgs {
     SplitArgs sk;
 };
 
+// The A / B tensor maps of a dgemm_tma_kernel launch: the multi-dimensional pair (one TMA
+// instruction each per stage; vec bit 1 tells the kernel) when the shape allows, else 2-D.
+template <class C>
+static int tma_maps(const LaunchArgs &a, CUtensorMap *ta, CUtensorMap *tb, int *vec) {
+    *vec = a.vec;
+    if (make_tmaps_md(ta, tb, a.A, a.M, a.K, a.lda, a.B, a.N, a.ldb, C::BM, C::BN, C::KG) == GEMM_OK) {
+        *vec |= 2;
+        return GEMM_OK;
+    }
+    int rc = make_tmap(ta, a.A, a.M, a.K, a.lda, C::BM);
+    if (rc) return rc;
+    return make_tmap(tb, a.B, a.K, a.N, a.ldb, 16);
+}
+
 struct CfgEntry {
     const char *name;
     gemm_cfg_desc d;
@@ -42,15 +59,14 @@ constexpr int kRotXP = 4;
 template <class C, int SPLIT, bool XP, int ROT = 1>
 static int launch_tma(const LaunchArgs &a, cudaStream_t st) {
     CUtensorMap ta, tb;
-    int rc = make_tmap(&ta, a.A, a.M, a.K, a.lda, C::BM);
-    if (rc) return rc;
-    rc = make_tmap(&tb, a.B, a.K, a.N, a.ldb, 16);
+    int vec = 0;
+    int rc = tma_maps<C>(a, &ta, &tb, &vec);
     if (rc) return rc;
     const int64_t tiles = ((int64_t)a.M + C::BM - 1) / C::BM * (((int64_t)a.N + C::BN - 1) / C::BN);
     if (tiles > 0x7FFFFFFF) return set_error(GEMM_ERR_UNSUPPORTED, "too many tiles (%lld)", (long long)tiles);
     dim3 grid((unsigned)tiles, SPLIT ? a.sk.splits : 1);
     return cuda_check(launch_k(dgemm_tma_kernel<C, SPLIT, XP, ROT>, grid, dim3(C::CONSUMER_THREADS), C::SMEM_BYTES, st,
-                               ta, tb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec, a.group_m, a.sk),
+                               ta, tb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, vec, a.group_m, a.sk),
                       "dgemm_tma_kernel launch");
 }
 
@@ -59,9 +75,8 @@ static int launch_tma(const LaunchArgs &a, cudaStream_t st) {
 template <class C>
 static int launch_tma_cluster(const LaunchArgs &a, cudaStream_t st) {
     CUtensorMap ta, tb;
-    int rc = make_tmap(&ta, a.A, a.M, a.K, a.lda, C::BM);
-    if (rc) return rc;
-    rc = make_tmap(&tb, a.B, a.K, a.N, a.ldb, 16);
+    int vec = 0;
+    int rc = tma_maps<C>(a, &ta, &tb, &vec);
     if (rc) return rc;
     const int64_t tiles = ((int64_t)a.M + C::BM - 1) / C::BM * (((int64_t)a.N + C::BN - 1) / C::BN);
     if (tiles > 0x7FFFFFFF) return set_error(GEMM_ERR_UNSUPPORTED, "too many tiles (%lld)", (long long)tiles);
@@ -70,7 +85,7 @@ static int launch_tma_cluster(const LaunchArgs &a, cudaStream_t st) {
     SplitArgs none{1, nullptr, nullptr};
     return cuda_check(launch_k_cluster(dgemm_tma_kernel<C, 2, false, kRotXP>, dim3((unsigned)tiles, S),
                                        dim3(C::CONSUMER_THREADS), C::SMEM_BYTES, st, 1u, (unsigned)S, ta, tb, a.M,
-                                       a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec, a.group_m, none),
+                                       a.N, a.K, a.alpha, a.beta, a.C, a.ldc, vec, a.group_m, none),
                       "dgemm_tma_kernel (cluster split-K) launch");
 }
 
@@ -92,9 +107,8 @@ constexpr int64_t kHybMinSteps = 16;   // hybrid tail: at least this many k-step
 template <class C>
 static int launch_streamk(const LaunchArgs &a, cudaStream_t st) {
     CUtensorMap ta, tb;
-    int rc = make_tmap(&ta, a.A, a.M, a.K, a.lda, C::BM);
-    if (rc) return rc;
-    rc = make_tmap(&tb, a.B, a.K, a.N, a.ldb, 16);
+    int vec = 0;
+    int rc = tma_maps<C>(a, &ta, &tb, &vec);
     if (rc) return rc;
     const int64_t tiles = ((int64_t)a.M + C::BM - 1) / C::BM * (((int64_t)a.N + C::BN - 1) / C::BN);
     const int64_t KT = ((int64_t)a.K + C::BK - 1) / C::BK;
@@ -107,7 +121,7 @@ static int launch_streamk(const LaunchArgs &a, cudaStream_t st) {
     rc = streamk_workspace(st, (size_t)C::BM * C::BN, grid, (size_t)tiles, &ws, &ctr);
     if (rc) return rc;
     return cuda_check(launch_k(dgemm_streamk_kernel<C>, dim3(grid), dim3(C::CONSUMER_THREADS), C::SMEM_BYTES, st,
-                               ta, tb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec, a.group_m, ws, ctr),
+                               ta, tb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, vec, a.group_m, ws, ctr),
                       "dgemm_streamk_kernel launch");
 }
 
@@ -126,9 +140,8 @@ static int launch_hybrid(const LaunchArgs &a, cudaStream_t st) {
                         "cudaFuncSetAttribute(hybrid data-parallel kernel)");
     if (rc) return rc;
     CUtensorMap ta, tb;
-    rc = make_tmap(&ta, a.A, a.M, a.K, a.lda, C::BM);
-    if (rc) return rc;
-    rc = make_tmap(&tb, a.B, a.K, a.N, a.ldb, 16);
+    int vec = 0;
+    rc = tma_maps<C>(a, &ta, &tb, &vec);
     if (rc) return rc;
     const int64_t tiles = ((int64_t)a.M + C::BM - 1) / C::BM * (((int64_t)a.N + C::BN - 1) / C::BN);
     const int64_t KT = ((int64_t)a.K + C::BK - 1) / C::BK;
@@ -139,7 +152,7 @@ static int launch_hybrid(const LaunchArgs &a, cudaStream_t st) {
     if (tdp > 0) {
         SplitArgs none{1, nullptr, nullptr};
         rc = cuda_check(launch_k(dgemm_tma_kernel<C, kDpSplit, kDpXP, kRotXP>, dim3((unsigned)tdp), dim3(C::CONSUMER_THREADS),
-                                 C::SMEM_BYTES, st, ta, tb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec,
+                                 C::SMEM_BYTES, st, ta, tb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, vec,
                                  a.group_m, none),
                         "hybrid data-parallel launch");
         if (rc || tail == 0) return rc;
@@ -151,7 +164,7 @@ static int launch_hybrid(const LaunchArgs &a, cudaStream_t st) {
     rc = streamk_workspace(st, (size_t)C::BM * C::BN, hy.gsk, 0, &hy.ws, &ctr);
     if (rc) return rc;
     rc = cuda_check(launch_k(dgemm_sktail_kernel<C>, dim3(hy.gsk), dim3(C::CONSUMER_THREADS), C::SMEM_BYTES, st, ta,
-                             tb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec, a.group_m, hy),
+                             tb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, vec, a.group_m, hy),
                     "dgemm_sktail_kernel launch");
     if (rc || ((int64_t)hy.gsk == tail && Ut % hy.gsk == 0)) return rc;   // every tail CTA had a whole tile
     static_assert((C::MB * C::NP) % kFixQ == 0, "fix-up quad split");
