@@ -7,6 +7,8 @@ exact dyadic regime, for integer work (index coverage, padding untouched) and fo
 invariants (determinism, all configurations agree).
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -793,3 +795,42 @@ def test_cluster_split_k_exact_regime_every_cfg(cuda_lib):
         for S in (2, 4, 7, 8, 16):   # 16 is clamped to the portable cluster size 8
             assert np.array_equal(run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=cfg, splits=S), ref), \
                 (cuda_lib.cfg_name(cfg), S)
+
+
+# ---------------------------------------------------------------- TMA staging variants (a2)
+_MD_SCRIPT = r"""
+import sys, hashlib, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import synth
+from paper_1706_10086_b200 import gemm as G
+out = []
+for (M, N, K, cfg, S) in [(1024, 1024, 1024, None, None), (640, 768, 512, "tma_64x64x32_w32x16_s3_splitk", 3),
+                          (2048, 1536, 1024, "tma_64x64x32_w32x16_s3_hybrid", None),
+                          (700, 1024, 2048, "tma_128x64x16_w32x16_s6_streamk", None),
+                          (512, 512, 4096, "tma_64x64x32_w32x16_s3_csplit", 4),
+                          (256, 1024, 512, "tma_256x64x16_w64x32_s4_xp", None)]:
+    A, B, C0 = synth.problem(M, N, K, seed=M + K)
+    dA, dB, dC = (torch.from_numpy(x).cuda() for x in (A, B, C0))
+    G.gemm(dA, dB, dC, 1.5, 0.5, cfg=None if cfg is None else G.cfg_id(cfg), splits=S)
+    torch.cuda.synchronize()
+    out.append(hashlib.sha256(dC.cpu().numpy().tobytes()).hexdigest())
+print(",".join(out))
+"""
+
+
+def test_multidim_tensor_maps_equal_2d_boxes_bitwise(cuda_lib):
+    """K and N multiples of 16 stage A and B with one 3-D / 4-D TMA box per stage instead of
+    KG * (1 + BN/16) 2-D boxes; the shared-memory image is the same, so every kernel family
+    (data-parallel, split-K, hybrid, stream-K, cluster split-K, XP) must give the same bits
+    with GEMM_TMA_MD=0 (2-D boxes forced) as with the default."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    runs = []
+    for md in ("1", "0"):
+        env = dict(os.environ, GEMM_TMA_MD=md)
+        p = subprocess.run([sys.executable, "-c", _MD_SCRIPT, root], capture_output=True, text=True, env=env,
+                           timeout=300)
+        assert p.returncode == 0, p.stderr[-2000:]
+        runs.append(p.stdout.strip().splitlines()[-1])
+    assert runs[0] == runs[1]
