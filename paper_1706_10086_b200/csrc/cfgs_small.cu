@@ -40,6 +40,14 @@ static const CfgEntry k_table[] = {
     DG_CSK(64, 64, 32, 32, 16, 3),
     DG_CSK(64, 64, 16, 32, 16, 6),
     DG_CSK(128, 64, 32, 32, 32, 3),
+    // EXPERIMENT: lone-CTA rate (XP split instance, deeper rings with one CTA per SM)
+    DG_TMA_SK(64, 64, 32, 32, 16, 3, 0, true, true, "_splitk_xp"),
+    DG_TMA_SK(64, 64, 32, 32, 16, 4, 0, true, false, "_splitk"),
+    DG_TMA_SK(64, 64, 32, 32, 16, 6, 0, true, true, "_splitk_xp"),
+    DG_TMA_SK(64, 64, 32, 16, 32, 4, 0, true, true, "_splitk_xp"),
+    DG_PSK(64, 64, 32, 32, 16, 6),
+    DG_PSK(64, 64, 32, 32, 16, 4),
+    DG_PSK(64, 64, 16, 32, 16, 8),
 };
 
 const CfgEntry *cfg_table_small(int *n) {
