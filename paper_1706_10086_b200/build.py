@@ -8,8 +8,6 @@ with torch (nvidia/nccl), and writes paper_1706_10086_b200/libgemm_f64.so.
 
 --trace builds an instrumented copy (-DDG_TRACE: per-CTA globaltimer timeline, see
 csrc/ptx.cuh) as libgemm_f64_trace.so for tools/trace_ctas.py; the product never loads it.
---debug-pair builds libgemm_f64_dbg.so (-DDG_PAIR_DEBUG: the pair stream-K kernel's ring waits
-report themselves and trap after 0.5 s instead of spinning forever).
 """
 
 from __future__ import annotations
@@ -27,8 +25,7 @@ LIB = os.path.join(HERE, "libgemm_f64.so")
 BUILD = os.path.join(HERE, "build")
 TRACE_LIB = os.path.join(HERE, "libgemm_f64_trace.so")
 TRACE_BUILD = os.path.join(HERE, "build_trace")
-DEBUG_LIB = os.path.join(HERE, "libgemm_f64_dbg.so")     # --debug-pair: bounded, reporting ring waits
-DEBUG_BUILD = os.path.join(HERE, "build_dbg")
+
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -66,16 +63,15 @@ def up_to_date(lib: str = LIB) -> bool:
     return all(os.path.getmtime(d) <= t for d in _deps())
 
 
-def build(force: bool = False, verbose: bool = False, trace: bool = False, debug: bool = False) -> str:
-    lib_out, build_dir = (TRACE_LIB, TRACE_BUILD) if trace else (DEBUG_LIB, DEBUG_BUILD) if debug else (LIB, BUILD)
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    lib_out, build_dir = (TRACE_LIB, TRACE_BUILD) if trace else (LIB, BUILD)
     if not force and up_to_date(lib_out):
         return lib_out
     os.makedirs(build_dir, exist_ok=True)
     nccl_inc, nccl_lib = _nccl_dirs()
     nvcc = _nvcc()
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-Xptxas", "-v",
-                    "-I", os.path.join(ROOT, "include"), "-I", nccl_inc] + (["-DDG_TRACE"] if trace else []) + \
-        (["-DDG_PAIR_DEBUG"] if debug else [])
+                    "-I", os.path.join(ROOT, "include"), "-I", nccl_inc] + (["-DDG_TRACE"] if trace else [])
 
     def compile_one(src):
         obj = os.path.join(build_dir, os.path.basename(src) + ".o")
@@ -103,4 +99,4 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False, debug
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True, trace="--trace" in sys.argv, debug="--debug-pair" in sys.argv)
+    build(force="--force" in sys.argv, verbose=True, trace="--trace" in sys.argv)

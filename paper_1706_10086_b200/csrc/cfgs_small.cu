@@ -1,4 +1,4 @@
-// cfgs_small.cu -- TMA configurations with 128x64 / 64x128 / 64x64 CTA tiles (mid-size and small problems;
+// cfgs_small.cu -- TMA configurations with 128x64 / 64x128 / 64x64 / 32x64 CTA tiles (mid-size and small problems;
 // 64x64 with E=16 is the paper's P100 optimum, 16x16 threads x T=4, Tab. 4).
 #include "registry.cuh"
 
@@ -40,14 +40,15 @@ static const CfgEntry k_table[] = {
     DG_CSK(64, 64, 32, 32, 16, 3),
     DG_CSK(64, 64, 16, 32, 16, 6),
     DG_CSK(128, 64, 32, 32, 32, 3),
-    // EXPERIMENT: lone-CTA rate (XP split instance, deeper rings with one CTA per SM)
-    DG_TMA_SK(64, 64, 32, 32, 16, 3, 0, true, true, "_splitk_xp"),
-    DG_TMA_SK(64, 64, 32, 32, 16, 4, 0, true, false, "_splitk"),
-    DG_TMA_SK(64, 64, 32, 32, 16, 6, 0, true, true, "_splitk_xp"),
-    DG_TMA_SK(64, 64, 32, 16, 32, 4, 0, true, true, "_splitk_xp"),
-    DG_PSK(64, 64, 32, 32, 16, 6),
-    DG_PSK(64, 64, 32, 32, 16, 4),
-    DG_PSK(64, 64, 16, 32, 16, 8),
+    // round 2: 32x64 / 64x32 / 32x32 tiles with E = 8 (16x16 warp tiles, 8 warps): twice the
+    // tiles of 64x64 at the same shape, so small problems fill the SMs with fewer (or no) split-K
+    // slices and no reduction (512^3: 128 tiles, one pass; DESIGN.md §6 small shapes, round 2)
+    DG_TMA_SPLIT(32, 64, 32, 16, 16, 3),
+    DG_TMA_SPLIT(32, 64, 32, 16, 16, 4),
+    DG_TMA_SPLIT(32, 64, 64, 16, 16, 3),
+    DG_TMA_SPLIT(64, 32, 32, 16, 16, 4),
+    DG_TMA_SPLIT(32, 32, 32, 16, 16, 4),
+    DG_TMA(32, 64, 32, 16, 16, 3),
 };
 
 const CfgEntry *cfg_table_small(int *n) {

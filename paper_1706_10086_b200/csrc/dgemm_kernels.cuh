@@ -31,9 +31,6 @@
 #include <cuda.h>
 
 #include "ptx.cuh"
-#ifdef DG_PAIR_DEBUG
-#include <cstdio>
-#endif
 
 namespace dg {
 
@@ -942,250 +939,6 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
                 stg_v4(mine + q * QSTRIDE, flat[4 * q], flat[4 * q + 1], flat[4 * q + 2], flat[4 * q + 3]);
         }
     }
-}
-
-// ------------------------------------------------------------------------------
-// Pair stream-K kernel (row a5, small and mid shapes).  One CTA per SM made of TWO consumer
-// groups of C::CONSUMER_WARPS warps that share one ring: local k-step l of the CTA's stream-K
-// range is multiplied by group l & 1 (STAGES even, so group g owns the ring slots of parity g).
-// Why: an SM needs two groups of 8 warps in their main loops to keep the DMMA pipe at ~99 %
-// (one alone reaches ~84-88 %), but two co-resident CTAs share the pipe unevenly and the one
-// that finishes first leaves the other alone (DESIGN.md §6 small shapes).  Here the groups are
-// coupled: the refill at the top of step l (issued by a lane of group l & 1) waits for the
-// OTHER group's release of step l - kLag, so neither group runs more than kLag k-steps ahead,
-// the pipe is shared evenly, and both groups reach every tile boundary together (kLag = 1
-// serialised the groups: each refill waited for the other group's step running beside it).
-// At the end of each tile segment the two partial sums are combined through shared memory,
-// p(group 0) + p(group 1) in that order, and each group keeps half of the m-blocks for the
-// epilogue or the stream-K partial (so the store work is split evenly as well).  Stream-K:
-// CTA g runs global k-steps [g*U/G, (g+1)*U/G) with G = SMs; a tile cut by CTA boundaries is
-// finished by the last-arriving CTA summing the segment partials in k order (as
-// dgemm_streamk_kernel).  Deterministic: the group of every k-step and the CTA ranges depend
-// only on the shape.
-template <class C>
-struct PairCfg {
-    static constexpr int GW = C::CONSUMER_WARPS;            // warps per group
-    static constexpr int THREADS = 2 * C::CONSUMER_THREADS;
-    static constexpr int HMB = C::MB / 2;                   // m-blocks per half
-    static constexpr int HQ = HMB * C::NP;                  // 256-bit quads per thread per half
-    static constexpr uint32_t XCH_BYTES = 2u * C::CONSUMER_THREADS * HQ * 32u;   // one half per direction
-    static constexpr uint32_t SMEM_BYTES = C::STAGES * C::STAGE_BYTES + XCH_BYTES + C::BAR_BYTES + 1024;
-    static_assert(C::STAGES % 2 == 0, "each group owns the ring slots of one parity");
-    static_assert(C::MB % 2 == 0, "the groups split the m-blocks in halves");
-};
-
-#ifdef DG_PAIR_DEBUG
-// debug builds only (build.py --debug-pair): a wait that reports itself and traps after 0.5 s
-__device__ __forceinline__ void pair_wait(uint64_t *bar, uint32_t parity, int what, int step) {
-    unsigned long long t0, t;
-    asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t0));
-    for (;;) {
-        uint32_t ok;
-        asm volatile(
-            "{\n.reg .pred P1;\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
-            : "=r"(ok)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-        if (ok) return;
-        asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t));
-        if (t - t0 > 500000000ull) {
-            printf("pair_wait timeout: cta %d warp %d lane %d %s step %d parity %u\n", (int)blockIdx.x,
-                   (int)(threadIdx.x >> 5), (int)(threadIdx.x & 31), what ? "full" : "empty", step, parity);
-            asm volatile("trap;");
-        }
-    }
-}
-#define DG_PAIR_WAIT(bar, par, what, step) pair_wait(bar, par, what, step)
-#else
-#define DG_PAIR_WAIT(bar, par, what, step) mbar_wait(bar, par)
-#endif
-
-template <class C>
-__global__ void __launch_bounds__(PairCfg<C>::THREADS, 1)
-    dgemm_pairsk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
-                        int N, int K, double alpha, double beta, double *__restrict__ Cm, int64_t ldc, int vec,
-                        int group_m, double *ws, int *counters) {
-    using P = PairCfg<C>;
-    constexpr int S = C::STAGES;
-    constexpr int kLag = 3;   // refill distance (odd, < S): step i refills the slot of step i - kLag
-    static_assert(kLag % 2 == 1 && kLag < S, "kLag");
-    extern __shared__ uint8_t smem_raw[];
-    const uint32_t raw = smem_u32(smem_raw);
-    const uint32_t base = (raw + 1023u) & ~1023u;
-    uint8_t *base_ptr = smem_raw + (base - raw);
-    const uint32_t xch = base + S * C::STAGE_BYTES;   // [direction][q][warp][lane][4 doubles]
-    uint64_t *full = reinterpret_cast<uint64_t *>(base_ptr + S * C::STAGE_BYTES + P::XCH_BYTES);
-    uint64_t *empty = full + S;
-    DG_TRACE_AT(0);
-
-    const int tiles_m = (M + C::BM - 1) / C::BM, tiles_n = (N + C::BN - 1) / C::BN;
-    const int KT = (K + C::BK - 1) / C::BK;
-    const int U = tiles_m * tiles_n * KT, G = gridDim.x, g = blockIdx.x;   // host: U < 2^31
-    const int u0 = (int)sk_bound(g, U, G), u1 = (int)sk_bound(g + 1, U, G);
-    const int nloc = u1 - u0;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int grp = warp / P::GW, wg = warp - grp * P::GW;
-    constexpr int R = 4 < P::GW ? 4 : P::GW;   // refilling warps per group
-    const uint64_t pol = (lane == 0 && wg < R) ? l2_policy_evict_normal() : 0;
-    auto issue_at = [&](int slot, int l) {
-        const int u = u0 + l;
-        const int t = u / KT;
-        int tm, tn;
-        tile_coords(t, tiles_m, tiles_n, group_m, tm, tn);
-        tma_issue_stage<C>(base_ptr + slot * C::STAGE_BYTES, &tmA, &tmB, &full[slot], tm * C::BM, tn * C::BN,
-                           u - t * KT, pol, (vec & 2) != 0);
-    };
-
-    if (threadIdx.x == 0) {
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], P::GW);   // a slot is read by one group
-        }
-        fence_mbar_init();
-        tma_prefetch_desc(&tmA);
-        tma_prefetch_desc(&tmB);
-    }
-    griddep_wait();
-    DG_TRACE_AT(1);
-    griddep_launch();
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < S && s < nloc; ++s) issue_at(s, s);
-    }
-    __syncthreads();
-
-    const int warp_m = wg / C::WARPS_N, warp_n = wg % C::WARPS_N;
-    const FragOffsets<C> fo(warp_m, warp_n, lane);
-    constexpr int Q = C::E / 4;
-    constexpr int64_t QSTRIDE = (int64_t)C::CONSUMER_WARPS * 32 * 4;
-    __shared__ int s_last_pair;
-    double acc[C::MB][C::NP][2][2];
-    double *flat = &acc[0][0][0][0];
-    int l = 0;   // local index of the current segment's first k-step
-    int tile = u0 / KT;
-    int kb = u0 - tile * KT;
-    while (l < nloc) {
-        const int ke = (u1 - tile * KT) < KT ? (u1 - tile * KT) : KT;
-        const int l_end = l + (ke - kb);
-#pragma unroll
-        for (int e = 0; e < C::E; ++e) flat[e] = 0.0;
-        // this group's k-steps of the segment: i = i0, i0 + 2, ...; ring slot s = i % S, lap parity ph
-        const int i0 = l + ((grp - l) & 1);
-        int s = i0 % S, ph = (i0 / S) & 1;
-        for (int i = i0; i < l_end; i += 2) {
-            if (lane == 0 && wg == ((i >> 1) % R) && i >= kLag && i - kLag + S < nloc) {
-                // refill the slot the other group released at step i - kLag with step i - kLag + S
-                // (kLag odd: the other group's slot; it couples the groups with kLag steps of slack)
-                const int sp = s >= kLag ? s - kLag : s - kLag + S;
-                DG_PAIR_WAIT(&empty[sp], (uint32_t)(s >= kLag ? ph : ph ^ 1), 0, i);
-                issue_at(sp, i - kLag + S);
-            }
-            __syncwarp();   // the refilling lane rejoins before the warp-wide mma.sync
-            DG_PAIR_WAIT(&full[s], (uint32_t)ph, 1, i);
-#ifdef DG_TRACE
-            if (i < 2) DG_TRACE_AT(2);
-#endif
-            const uint32_t sA = base + s * C::STAGE_BYTES;
-            mma_stage<C>(sA, sA + C::A_BYTES, fo, acc);
-            release_slot(&empty[s], lane);
-            s += 2;
-            if (s >= S) {
-                s -= S;
-                ph ^= 1;
-            }
-        }
-        // combine: group grp keeps the quads q with q / HQ == grp (m-blocks [grp*HMB, (grp+1)*HMB))
-        // and hands the other half over; quad indices stay compile-time (registers, no stack)
-        __syncthreads();   // the previous segment's exchange has been read by everyone
-#pragma unroll
-        for (int q = 0; q < Q; ++q) {
-            if (q / P::HQ != grp) {
-                const uint32_t a = xch + (uint32_t)((((grp * P::HQ + q % P::HQ) * P::GW + wg) * 32 + lane) * 32);
-                sts_v2(a, flat[4 * q], flat[4 * q + 1]);
-                sts_v2(a + 16, flat[4 * q + 2], flat[4 * q + 3]);
-            }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int q = 0; q < Q; ++q) {
-            if (q / P::HQ == grp) {
-                const uint32_t a =
-                    xch + (uint32_t)(((((1 - grp) * P::HQ + q % P::HQ) * P::GW + wg) * 32 + lane) * 32);
-                double v[4];
-                asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v[0]), "=d"(v[1]) : "r"(a));
-                asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v[2]), "=d"(v[3]) : "r"(a + 16));
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const double x = flat[4 * q + e];
-                    flat[4 * q + e] = grp == 0 ? x + v[e] : v[e] + x;   // p(group 0) + p(group 1)
-                }
-            }
-        }
-        // stream-K segments of this tile: CTA boundaries strictly inside (tile*KT, (tile+1)*KT)
-        const int t0 = tile * KT;
-        const int before = (int)sk_count_le(t0, U, G);
-        const int nseg = (int)sk_count_le(t0 + KT - 1, U, G) - before + 1;
-        bool do_epi = true;
-        if (nseg > 1) {
-            const int my_slot = 2 * g + ((t0 + kb) == u0 ? 0 : 1);
-            double *mine = partial_slot<C>(ws, my_slot, wg, lane);
-#pragma unroll
-            for (int q = 0; q < Q; ++q)
-                if (q / P::HQ == grp)
-                    stg_v4(mine + q * QSTRIDE, flat[4 * q], flat[4 * q + 1], flat[4 * q + 2], flat[4 * q + 3]);
-            __threadfence();
-            __syncthreads();
-            if (threadIdx.x == 0) s_last_pair = (atomicAdd(&counters[tile], 1) == nseg - 1);
-            __syncthreads();
-            do_epi = s_last_pair != 0;
-            if (do_epi) {
-                __threadfence();
-                // segment order = k order: segment j of the tile comes from CTA before - 1 + j
-#pragma unroll
-                for (int e = 0; e < C::E; ++e) flat[e] = 0.0;
-                for (int j = 0; j < nseg; ++j) {
-                    const int gj = before - 1 + j;
-                    const int slot = 2 * gj + (sk_bound(gj, U, G) >= t0 ? 0 : 1);
-                    const double *src = partial_slot<C>(ws, slot, wg, lane);
-#pragma unroll
-                    for (int q = 0; q < Q; ++q) {
-                        if (q / P::HQ == grp) {
-                            double v0, v1, v2, v3;
-                            asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];\n"
-                                         : "=d"(v0), "=d"(v1), "=d"(v2), "=d"(v3)
-                                         : "l"(src + q * QSTRIDE));
-                            flat[4 * q] += v0;
-                            flat[4 * q + 1] += v1;
-                            flat[4 * q + 2] += v2;
-                            flat[4 * q + 3] += v3;
-                        }
-                    }
-                }
-                if (threadIdx.x == 0) counters[tile] = 0;   // ready for the next launch on this stream
-            }
-        }
-        if (do_epi) {
-            int tm, tn;
-            tile_coords(tile, tiles_m, tiles_n, group_m, tm, tn);
-            const int row0 = tm * C::BM + warp_m * C::WM + (lane >> 2);
-            const int col0 = tn * C::BN + warp_n * C::WN + 4 * (lane & 3);
-#pragma unroll
-            for (int q = 0; q < Q; ++q) {
-                if (q / P::HQ == grp) {
-                    const int mb = q / C::NP, np = q - mb * C::NP;
-                    const double w[4] = {flat[4 * q], flat[4 * q + 2], flat[4 * q + 1], flat[4 * q + 3]};
-                    epilogue_quad(w, row0 + mb * 8, col0 + np * 16, M, N, alpha, beta, Cm, ldc, (vec & 1) != 0);
-                }
-            }
-        }
-        ++tile;
-        kb = 0;
-        l = l_end;
-    }
-    DG_TRACE_AT(6);
-#ifdef DG_TRACE
-    DG_TRACE_SLOT(7, (unsigned long long)dg_smid());
-#endif
 }
 
 constexpr int kFixQ = 4;   // quads per fix-up CTA (grid.y = MB*NP / kFixQ)

@@ -330,6 +330,10 @@ static const Cand k_tma_cands[] = {
     {"tma_64x64x16_w32x16_s6_splitk", 0.992},  {"tma_128x64x16_w32x16_s6_splitk", 0.982},
     {"tma_64x128x16_w32x64_s4_splitk", 0.981}, {"tma_128x128x16_w32x32_s4_splitk", 0.971},
     {"tma_128x64x16_w32x16_s6_streamk", 0.920}, {"tma_64x64x16_w32x16_s6_streamk", 0.852},
+    // round 2: 32x64 / 64x32 tiles, E = 8 (steady state 0.97-0.99 of the roof at 4096^3-8192^3,
+    // profiles/r02/small_tiles_cfgs_v1.jsonl); they win the small shapes by needing fewer slices
+    {"tma_32x64x32_w16x16_s3_splitk", 0.985},  {"tma_32x64x64_w16x16_s3_splitk", 0.985},
+    {"tma_64x32x32_w16x16_s4_splitk", 0.980},
 };
 
 struct Choice {

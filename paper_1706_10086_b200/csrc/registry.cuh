@@ -125,29 +125,6 @@ static int launch_streamk(const LaunchArgs &a, cudaStream_t st) {
                       "dgemm_streamk_kernel launch");
 }
 
-// Pair stream-K launch: one 2-group CTA per SM (grid = min(SMs, U)); workspace = 2 partial
-// slots per CTA, counters per tile (as launch_streamk).
-template <class C>
-static int launch_pairsk(const LaunchArgs &a, cudaStream_t st) {
-    CUtensorMap ta, tb;
-    int vec = 0;
-    int rc = tma_maps<C>(a, &ta, &tb, &vec);
-    if (rc) return rc;
-    const int64_t tiles = ((int64_t)a.M + C::BM - 1) / C::BM * (((int64_t)a.N + C::BN - 1) / C::BN);
-    const int64_t KT = ((int64_t)a.K + C::BK - 1) / C::BK;
-    if (tiles * KT > 0x7FFFFFFF) return set_error(GEMM_ERR_UNSUPPORTED, "stream-K needs tiles*k-steps < 2^31");
-    const int grid = streamk_grid((const void *)dgemm_pairsk_kernel<C>, PairCfg<C>::THREADS, PairCfg<C>::SMEM_BYTES,
-                                  tiles * KT);
-    if (grid <= 0) return set_error(GEMM_ERR_CUDA, "pair stream-K occupancy query failed");
-    double *ws = nullptr;
-    int *ctr = nullptr;
-    rc = streamk_workspace(st, (size_t)C::BM * C::BN, grid, (size_t)tiles, &ws, &ctr);
-    if (rc) return rc;
-    return cuda_check(launch_k(dgemm_pairsk_kernel<C>, dim3(grid), dim3(PairCfg<C>::THREADS), PairCfg<C>::SMEM_BYTES,
-                               st, ta, tb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, vec, a.group_m, ws, ctr),
-                      "dgemm_pairsk_kernel launch");
-}
-
 // Hybrid launch: the W full data-parallel waves as one plain XP launch (grid = W*G tiles),
 // then the tail's k-steps over gsk stream-K CTAs, then the fix-up of the cut tail tiles.
 template <class C>
@@ -210,13 +187,6 @@ static int launch_hybrid(const LaunchArgs &a, cudaStream_t st) {
                            (int)Cfg<BM, BN, BK, WM, WN, ST>::SMEM_BYTES, 1, -1, 0},                           \
              (const void *)dgemm_streamk_kernel<Cfg<BM, BN, BK, WM, WN, ST>>,                                 \
              launch_streamk<Cfg<BM, BN, BK, WM, WN, ST>>}
-
-#define DG_PSK(BM, BN, BK, WM, WN, ST)                                                                    \
-    CfgEntry{"tma_" #BM "x" #BN "x" #BK "_w" #WM "x" #WN "_s" #ST "_pairsk",                                  \
-             gemm_cfg_desc{BM, BN, BK, WM, WN, ST, PairCfg<Cfg<BM, BN, BK, WM, WN, ST>>::THREADS,              \
-                           (int)PairCfg<Cfg<BM, BN, BK, WM, WN, ST>>::SMEM_BYTES, 1, -1, 0},                  \
-             (const void *)dgemm_pairsk_kernel<Cfg<BM, BN, BK, WM, WN, ST>>,                                  \
-             launch_pairsk<Cfg<BM, BN, BK, WM, WN, ST>>}
 
 // cluster split-K: split_k = -3 (slices chosen per call, reduced through distributed shared memory)
 #define DG_CSK(BM, BN, BK, WM, WN, ST)                                                                    \

@@ -101,8 +101,7 @@ def test_cfg_registry(G):
     for info in G.cfgs():
         names.add(info["name"])
         assert info["bm"] % info["wm"] == 0 and info["bn"] % info["wn"] == 0
-        groups = 2 if info["name"].endswith("_pairsk") else 1   # pair stream-K: two consumer groups per CTA
-        assert info["threads"] == groups * 32 * (info["bm"] // info["wm"]) * (info["bn"] // info["wn"])
+        assert info["threads"] == 32 * (info["bm"] // info["wm"]) * (info["bn"] // info["wn"])
         assert info["smem_bytes"] <= 227 * 1024
         stage = 8 * (info["bm"] + info["bn"]) * info["bk"]      # Eq. (5) analog: 2 tiles per stage
         assert info["smem_bytes"] >= info["stages"] * stage
