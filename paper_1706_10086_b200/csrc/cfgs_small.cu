@@ -49,6 +49,8 @@ static const CfgEntry k_table[] = {
     DG_TMA_SPLIT(64, 32, 32, 16, 16, 4),
     DG_TMA_SPLIT(32, 32, 32, 16, 16, 4),
     DG_TMA(32, 64, 32, 16, 16, 3),
+    DG_HYB(32, 64, 32, 16, 16, 3),
+    DG_SK(32, 64, 32, 16, 16, 3),
 };
 
 const CfgEntry *cfg_table_small(int *n) {

@@ -941,9 +941,11 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, C::MIN_BLOCKS)
     }
 }
 
-constexpr int kFixQ = 4;   // quads per fix-up CTA (grid.y = MB*NP / kFixQ)
+constexpr int kFixQ = 4;   // quads per fix-up CTA (grid.y = MB*NP / FixQ<C>), fewer for E = 8 tiles
+template <class C>
+constexpr int FixQ = (C::MB * C::NP) < kFixQ ? (C::MB * C::NP) : kFixQ;
 
-// Tail fix-up: one CTA per (tail tile, kFixQ quads); a tile cut between CTAs gets the sum of its
+// Tail fix-up: one CTA per (tail tile, FixQ<C> quads); a tile cut between CTAs gets the sum of its
 // partials in k order (CTA jlo's segment first), then the plain epilogue.
 template <class C>
 __global__ void __launch_bounds__(C::CONSUMER_THREADS, 1)
@@ -967,28 +969,28 @@ __global__ void __launch_bounds__(C::CONSUMER_THREADS, 1)
     const int row0 = tm * C::BM + warp_m * C::WM + (lane >> 2);
     const int col0 = tn * C::BN + warp_n * C::WN + 4 * (lane & 3);
     // quad q = mb * NP + np holds flat accumulators 4q..4q+3 = acc[mb][np][j][i] (j major).
-    // blockIdx.y selects kFixQ quads; their kFixQ loads per partial are issued together so
+    // blockIdx.y selects FixQ<C> quads; their FixQ<C> loads per partial are issued together so
     // the sum costs ~nseg memory round trips, not nseg * quads.
-    const int qb = blockIdx.y * kFixQ;
-    double x[kFixQ][4];
+    const int qb = blockIdx.y * FixQ<C>;
+    double x[FixQ<C>][4];
 #pragma unroll
-    for (int u = 0; u < kFixQ; ++u) x[u][0] = x[u][1] = x[u][2] = x[u][3] = 0.0;
+    for (int u = 0; u < FixQ<C>; ++u) x[u][0] = x[u][1] = x[u][2] = x[u][3] = 0.0;
     for (int j = jlo; j <= jhi; ++j) {
         const int slot = 2 * j + (sk_bound(j, Ut, gsk) >= t0 ? 0 : 1);
         const double *src = partial_slot<C>(const_cast<double *>(ws), slot, warp, lane) + qb * QSTRIDE;
-        double v[kFixQ][4];
+        double v[FixQ<C>][4];
 #pragma unroll
-        for (int u = 0; u < kFixQ; ++u)
+        for (int u = 0; u < FixQ<C>; ++u)
             asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];\n"
                          : "=d"(v[u][0]), "=d"(v[u][1]), "=d"(v[u][2]), "=d"(v[u][3])
                          : "l"(src + u * QSTRIDE));
 #pragma unroll
-        for (int u = 0; u < kFixQ; ++u)
+        for (int u = 0; u < FixQ<C>; ++u)
 #pragma unroll
             for (int e = 0; e < 4; ++e) x[u][e] += v[u][e];
     }
 #pragma unroll
-    for (int u = 0; u < kFixQ; ++u) {
+    for (int u = 0; u < FixQ<C>; ++u) {
         const int q = qb + u;
         const int mb = q / C::NP, np = q - mb * C::NP;
         const double w[4] = {x[u][0], x[u][2], x[u][1], x[u][3]};   // (j,i) = (0,0), (1,0), (0,1), (1,1)

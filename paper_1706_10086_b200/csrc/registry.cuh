@@ -167,8 +167,8 @@ static int launch_hybrid(const LaunchArgs &a, cudaStream_t st) {
                              tb, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, vec, a.group_m, hy),
                     "dgemm_sktail_kernel launch");
     if (rc || ((int64_t)hy.gsk == tail && Ut % hy.gsk == 0)) return rc;   // every tail CTA had a whole tile
-    static_assert((C::MB * C::NP) % kFixQ == 0, "fix-up quad split");
-    return cuda_check(launch_k(dgemm_hybrid_fixup_kernel<C>, dim3((unsigned)tail, C::MB * C::NP / kFixQ),
+    static_assert((C::MB * C::NP) % FixQ<C> == 0, "fix-up quad split");
+    return cuda_check(launch_k(dgemm_hybrid_fixup_kernel<C>, dim3((unsigned)tail, C::MB * C::NP / FixQ<C>),
                                dim3(C::CONSUMER_THREADS), 0, st, a.M, a.N, a.K, a.alpha, a.beta, a.C, a.ldc, a.vec,
                                a.group_m, (int)tdp, hy.gsk, (const double *)hy.ws),
                       "dgemm_hybrid_fixup_kernel launch");

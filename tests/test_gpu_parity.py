@@ -696,6 +696,20 @@ def test_hybrid_exact_regime_bitwise(cuda_lib):
     assert np.array_equal(run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=hyb), ref)
 
 
+@pytest.mark.parametrize("shape", [(1000, 2500, 1000), (300, 200, 2000), (1024, 1024, 1024)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_hybrid_every_cfg_exact_regime_bitwise(cuda_lib, shape):
+    """Every hybrid configuration (incl. the E = 8 32x64 tiles, whose fix-up CTAs take 2 quads
+    instead of 4) against the oracle bit for bit in the exact regime, cut tail tiles included."""
+    M, N, K = shape
+    A, B, C0 = synth.problem(M, N, K, mode="dyadic", seed=M + 7)
+    ref = oracle.dgemm(1.5, A, B, 0.5, C0)
+    hybs = [c["id"] for c in cuda_lib.cfgs() if c["split_k"] == -2]
+    assert len(hybs) >= 4
+    for cfg in hybs:
+        assert np.array_equal(run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, cfg=cfg), ref), cuda_lib.cfg_name(cfg)
+
+
 def _tile_coords(bid, tiles_m, tiles_n, group_m=8):
     per = group_m * tiles_n
     grp, r = divmod(bid, per)
@@ -742,6 +756,9 @@ def test_hybrid_plan_full_size_tail_rows(cuda_lib, shape):
                                              ("tma_64x64x16_w32x16_s6_hybrid", None),
                                              ("tma_128x64x16_w32x16_s6_streamk", None),
                                              ("tma_64x64x32_w32x16_s3_csplit", 4), ("tma_64x64x16_w32x16_s6_csplit", 8),
+                                             ("tma_32x64x32_w16x16_s3_splitk", 2), ("tma_32x64x64_w16x16_s3_splitk", 1),
+                                             ("tma_64x32x32_w16x16_s4_splitk", 3), ("tma_32x32x32_w16x16_s4_splitk", 4),
+                                             ("tma_32x64x32_w16x16_s3", None),
                                              ])
 def test_ring_slot_reuse_exact_k_signature(cuda_lib, cfg_name, splits):
     """Regression for the ring's write-after-read hazard (DESIGN.md §6 "Releasing a slot"):
