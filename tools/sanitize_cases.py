@@ -42,10 +42,11 @@ def main():
     A = torch.rand((M, K), dtype=torch.float64, device="cuda")
     B = torch.rand((K, N), dtype=torch.float64, device="cuda")
     C = torch.zeros((M, N), dtype=torch.float64, device="cuda")
-    hyb = G.cfg_id("tma_256x64x16_w64x32_s4_hybrid")
-    assert G.launches_per_call(hyb, M, N, K, sms) == 3
-    G.gemm(A, B, C, 1.0, 0.0, cfg=hyb)
-    n += 1
+    assert G.launches_per_call(G.cfg_id("tma_256x64x16_w64x32_s4_hybrid"), M, N, K, sms) == 3
+    for info in G.cfgs():                    # every hybrid configuration (32x64: 2-quad fix-up CTAs)
+        if info["split_k"] == -2:
+            G.gemm(A, B, C, 1.0, 0.0, cfg=info["id"])
+            n += 1
     # repack path: large problem with odd leading dimensions
     M, N, K = 1200, 1201, 1501
     A = torch.rand((M, K), dtype=torch.float64, device="cuda")
