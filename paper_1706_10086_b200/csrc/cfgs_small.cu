@@ -51,6 +51,11 @@ static const CfgEntry k_table[] = {
     DG_TMA(32, 64, 32, 16, 16, 3),
     DG_HYB(32, 64, 32, 16, 16, 3),
     DG_SK(32, 64, 32, 16, 16, 3),
+    // three CTAs per SM (64 registers; tuner-only: with three slots per SM the block scheduler packs
+    // a grid that fits onto fewer SMs, DESIGN.md §6 small shapes (10))
+    DG_TMA_SPLIT_MB(32, 64, 32, 16, 16, 3, 3),
+    DG_TMA_MB(32, 64, 32, 16, 16, 3, 3),
+    DG_TMA_SPLIT_MB(32, 64, 32, 16, 16, 2, 3),
 };
 
 const CfgEntry *cfg_table_small(int *n) {

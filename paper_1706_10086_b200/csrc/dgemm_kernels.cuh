@@ -34,7 +34,7 @@
 
 namespace dg {
 
-template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_>
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, int MINB_ = 0>
 struct Cfg {
     static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_;
     static_assert(BM % WM == 0 && BN % WN == 0, "warp tiles must tile the CTA tile");
@@ -58,7 +58,10 @@ struct Cfg {
     static constexpr uint32_t BAR_BYTES = 2 * STAGES * 8;
     static constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + BAR_BYTES + 1024;  // +1024: manual alignment
     // two CTAs per SM when shared memory allows it (227 KB per SM usable, ~1 KB reserved per CTA)
-    static constexpr int MIN_BLOCKS = (2 * (SMEM_BYTES + 1024) <= 228 * 1024) ? 2 : 1;
+    // MINB_ > 0: the launch-bounds occupancy is forced (3 CTAs per SM for the E = 8 tiles, whose
+    // one-per-SM register budget would otherwise stop at two)
+    static constexpr int MINB = MINB_;
+    static constexpr int MIN_BLOCKS = MINB_ > 0 ? MINB_ : (2 * (SMEM_BYTES + 1024) <= 228 * 1024) ? 2 : 1;
 };
 
 // k-permutation inside a 16-deep k-group.  A thread with MMA k-index t (= lane & 3)
@@ -302,7 +305,9 @@ __device__ __forceinline__ void sum_partials(double (&acc)[C::MB][C::NP][2][2], 
                                              SlotOf slot_of, int warp, int lane) {
     constexpr int Q = C::E / 4;
     constexpr int64_t QSTRIDE = (int64_t)C::CONSUMER_WARPS * 32 * 4;   // doubles between q groups
-    constexpr int PB0 = C::E >= 32 ? 1 : 32 / C::E;
+    // E = 16: 2 partials x 4 quads in flight; E = 8: 4 x 2, or 2 x 2 in the 3-CTA/SM instances
+    // (64 registers: the four-partial batch alone held 32 doubles)
+    constexpr int PB0 = C::E >= 32 ? 1 : C::MINB >= 3 ? 2 : 32 / C::E;
     constexpr int PB = PB0 < PB_MAX ? PB0 : PB_MAX;                   // partials in flight
     constexpr int QC = Q < 8 ? Q : 8;                                  // q groups in flight
     static_assert(Q % QC == 0, "q chunking");

@@ -213,6 +213,15 @@ static int launch_hybrid(const LaunchArgs &a, cudaStream_t st) {
                            (int)Cfg<BM, BN, BK, WM, WN, ST>::SMEM_BYTES, 1, 1, 0},                            \
              (const void *)dgemm_tma_kernel<Cfg<BM, BN, BK, WM, WN, ST>, false, true, kRotXP>,                 \
              launch_tma<Cfg<BM, BN, BK, WM, WN, ST>, false, true, kRotXP>}
+// split-K / plain instances with a forced launch-bounds occupancy MB (name suffix _mbMB)
+#define DG_TMA_MB_SK(BM, BN, BK, WM, WN, ST, MB, SK, SPLIT, SUFFIX)                                          \
+    CfgEntry{"tma_" #BM "x" #BN "x" #BK "_w" #WM "x" #WN "_s" #ST SUFFIX "_mb" #MB,                           \
+             gemm_cfg_desc{BM, BN, BK, WM, WN, ST, Cfg<BM, BN, BK, WM, WN, ST, MB>::CONSUMER_THREADS,          \
+                           (int)Cfg<BM, BN, BK, WM, WN, ST, MB>::SMEM_BYTES, 1, SK, 0},                       \
+             (const void *)dgemm_tma_kernel<Cfg<BM, BN, BK, WM, WN, ST, MB>, SPLIT, false, kRotXP>,            \
+             launch_tma<Cfg<BM, BN, BK, WM, WN, ST, MB>, SPLIT, false, kRotXP>}
+#define DG_TMA_SPLIT_MB(BM, BN, BK, WM, WN, ST, MB) DG_TMA_MB_SK(BM, BN, BK, WM, WN, ST, MB, 0, true, "_splitk")
+#define DG_TMA_MB(BM, BN, BK, WM, WN, ST, MB) DG_TMA_MB_SK(BM, BN, BK, WM, WN, ST, MB, 1, false, "")
 #define DG_GEN(BM, BN, BK, WM, WN, ST)                                                                       \
     CfgEntry{"gen_" #BM "x" #BN "x" #BK "_w" #WM "x" #WN "_s" #ST,                                            \
              gemm_cfg_desc{BM, BN, BK, WM, WN, ST, Cfg<BM, BN, BK, WM, WN, ST>::CONSUMER_THREADS,              \
