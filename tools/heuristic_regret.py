@@ -20,10 +20,11 @@ from paper_1706_10086_b200 import gemm as G  # noqa: E402
 from paper_1706_10086_b200 import tuner  # noqa: E402
 
 
-def shapes(n, seed):
+def shapes(n, seed, lo=500, hi=6000):
     rng = np.random.default_rng(seed)
-    out = [tuple(int(x) for x in rng.integers(500, 6001, 3)) for _ in range(n)]
-    out += [(256, 8192, 8192), (8192, 256, 8192), (4096, 4096, 512), (640, 640, 40000), (12000, 12000, 1000)]
+    out = [tuple(int(x) for x in rng.integers(lo, hi + 1, 3)) for _ in range(n)]
+    if (lo, hi) == (500, 6000):
+        out += [(256, 8192, 8192), (8192, 256, 8192), (4096, 4096, 512), (640, 640, 40000), (12000, 12000, 1000)]
     return out
 
 
@@ -32,11 +33,13 @@ def main():
     ap.add_argument("--n", type=int, default=16)
     ap.add_argument("--seed", type=int, default=7)
     ap.add_argument("--out", default="gpurun_out/regret.csv")
+    ap.add_argument("--lo", type=int, default=500, help="shape range (small shapes: --lo 200 --hi 1600)")
+    ap.add_argument("--hi", type=int, default=6000)
     a = ap.parse_args()
     with open(a.out, "w", newline="") as f:
         w = csv.writer(f)
         w.writerow(["m", "n", "k", "plan", "plan_splits", "plan_tflops", "best", "best_splits", "best_tflops", "regret"])
-        for (M, N, K) in shapes(a.n, a.seed):
+        for (M, N, K) in shapes(a.n, a.seed, a.lo, a.hi):
             Ke, Ne = K + (K & 1), N + (N & 1)        # even leading dimensions: the TMA path
             A = torch.empty((M, Ke), dtype=torch.float64, device="cuda")[:, :K]
             B = torch.empty((K, Ne), dtype=torch.float64, device="cuda")[:, :N]
