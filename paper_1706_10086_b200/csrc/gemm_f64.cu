@@ -331,9 +331,14 @@ static const Cand k_tma_cands[] = {
     {"tma_64x128x16_w32x64_s4_splitk", 0.981}, {"tma_128x128x16_w32x32_s4_splitk", 0.971},
     {"tma_128x64x16_w32x16_s6_streamk", 0.920}, {"tma_64x64x16_w32x16_s6_streamk", 0.852},
     // round 2: 32x64 / 64x32 tiles, E = 8 (steady state 0.97-0.99 of the roof at 4096^3-8192^3,
-    // profiles/r02/small_tiles_cfgs_v1.jsonl); they win the small shapes by needing fewer slices
-    {"tma_32x64x32_w16x16_s3_splitk", 0.985},  {"tma_32x64x64_w16x16_s3_splitk", 0.985},
-    {"tma_64x32x32_w16x16_s4_splitk", 0.980},
+    // profiles/r02/small_tiles_cfgs_v1.jsonl); they win the small shapes by needing fewer slices.
+    // One CTA per SM (32x64x64, 144 KB) runs at a lone 8-warp CTA's ~0.95 (lone_cta_rate_v1.jsonl);
+    // 32x32 tiles move twice the shared-memory bytes per FLOP and a 2-stage ring hides less
+    // latency on long k-ranges (charged 0.90 / 0.96: measured to lose mid shapes with more,
+    // profiles/r02/regret_seed23_m2.csv)
+    {"tma_32x64x32_w16x16_s3_splitk", 0.985},  {"tma_32x64x64_w16x16_s3_splitk", 0.950},
+    {"tma_64x32x32_w16x16_s4_splitk", 0.980},  {"tma_32x32x32_w16x16_s4_splitk", 0.900},
+    {"tma_32x64x32_w16x16_s3_splitk_mb3", 0.985}, {"tma_32x64x32_w16x16_s2_splitk_mb3", 0.960},
 };
 
 struct Choice {
@@ -345,19 +350,34 @@ static double est_time(const gemm_cfg_desc &d, int occ, int sms, int64_t M, int6
                        double eff) {
     const int64_t tiles = ((M + d.bm - 1) / d.bm) * ((N + d.bn - 1) / d.bn);
     const int64_t KT = (K + d.bk - 1) / d.bk;
-    // quantised per SM, not per CTA slot: the CTAs an SM holds share its DMMA pipe, so an SM
-    // that ends with one CTA instead of two finishes it in about half the time (with
-    // ceil(CTAs / (SMs x occupancy)) full slot-waves the model over-charged short split-K
-    // waves of the two-CTA-per-SM tiles by up to 9 %, r01_heuristic_regret_v5_*.csv)
-    // ... but a CTA of a two-per-SM tile that is alone on its SM runs at only ~60 % of the SM's
-    // DMMA rate, so a grid that cannot give any SM a second CTA is charged for that.
-    const int64_t per_sm = (tiles * S + sms - 1) / sms;
-    const double lone = (occ > 1 && tiles * S <= sms) ? 1.0 / 0.6 : 1.0;
+    // Rounds of CTAs, counted per SM: the `occ` CTAs an SM holds share its DMMA pipe, so a full
+    // round of SMs x occ CTAs costs occ CTA-times.  The last, partial round of m CTAs puts c
+    // CTAs on an SM; with c >= 2 they still fill the pipe (c CTA-times), but a CTA alone on its SM
+    // (c = 1) runs a short k-range at only ~60 % of the SM's rate (ramp and fill, per-CTA traces),
+    // so it is charged 1/0.6.  Round 1 charged that only when every CTA was alone and otherwise
+    // ceil(CTAs / SMs), which sent small shapes to one-pass plans that end on lone CTAs (round 2
+    // heuristic regret up to 23 % on unseen shapes, profiles/r02/regret_small_seed5.csv).  With
+    // three or more slots per SM the block scheduler packs a grid that fits into one round onto
+    // fewer SMs (768^3: 288 CTAs on 113 SMs, profiles/r02/trace_ctas_e8_occupancy_v1.jsonl), so
+    // such a round is charged as if every used SM held occ CTAs.  occ == 1 kernels (one CTA per SM
+    // by design) have their lone rate in eff.
+    const int64_t n = tiles * S, slots = (int64_t)sms * occ;
+    const int64_t full = n / slots, m = n - full * slots;
+    double units = (double)(full * occ);
+    if (m > 0) {
+        if (occ == 1) {
+            units += 1.0;
+        } else {
+            int64_t c = (m + sms - 1) / sms;
+            if (full == 0 && occ >= 3) c = occ;
+            units += c >= 2 ? (double)c : 1.0 / 0.6;
+        }
+    }
     // fixed costs are counted in 16-deep k-steps (pipeline fill, epilogue, split reduction),
     // so a BK = 32 stage is charged half as many of its own steps
     const double u = 16.0 / d.bk;
     const double ksteps = (double)((KT + S - 1) / S) + (4.0 + (S > 1 ? 2.0 : 0.0)) * u;
-    return (double)per_sm * lone * d.bm * d.bn * ksteps * (d.bk / 16.0) / eff;
+    return units * d.bm * d.bn * ksteps * (d.bk / 16.0) / eff;
 }
 
 static Choice choose_uncached(int64_t M, int64_t N, int64_t K, bool tma, bool single_pass);
