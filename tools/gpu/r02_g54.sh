@@ -1,0 +1,14 @@
+# re-entry verification at HEAD (rebuilt container): GPU suite, smoke, bench N=1, torchrun N=1, reference arm
+set -x
+nvidia-smi --query-gpu=name,clocks.max.sm,power.limit --format=csv
+timeout -s KILL 1500 python -m pytest tests -m gpu -x -q > gpurun_out/r02_gpu_tests_full_v8.txt 2>&1
+echo tests rc=$?
+tail -1 gpurun_out/r02_gpu_tests_full_v8.txt
+timeout -s KILL 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/r02_smoke_v8.txt 2>&1
+echo smoke rc=$?
+timeout -s KILL 900 python bench.py > gpurun_out/r02_bench_n1_v7.json 2> gpurun_out/r02_bench_n1_v7.err
+cat gpurun_out/r02_bench_n1_v7.json
+timeout -s KILL 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 1 --steps 5 --warmup 3 > gpurun_out/r02_bench_torchrun_n1_v7.txt 2> gpurun_out/r02_bench_torchrun_n1_v7.err
+cat gpurun_out/r02_bench_torchrun_n1_v7.txt
+timeout -s KILL 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/r02_bench_reference_v7.json 2> gpurun_out/r02_bench_reference_v7.err
+cat gpurun_out/r02_bench_reference_v7.json
