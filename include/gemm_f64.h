@@ -204,6 +204,35 @@ GEMM_API int gemm_plan_ex(int64_t M, int64_t N, int64_t K, const double *A, int6
 GEMM_API int gemm_plan_set(int64_t M, int64_t N, int64_t K, int tma, int cfg_id, int splits);
 GEMM_API int gemm_plan_clear(void);
 GEMM_API int gemm_tune_load(const char *path, int *n_loaded);
+/* Writes every pinned plan (gemm_plan_set, gemm_tune_load, gemm_plan_autotune) to `path` in
+ * gemm_tune_load's format, replacing the file; *n_saved (may be NULL) = lines written.
+ * NULL path / unwritable file -> GEMM_ERR_ARG. */
+GEMM_API int gemm_tune_save(const char *path, int *n_saved);
+
+/* Run-time tuning of one shape (§2.3 P:315-320 done at first use instead of offline): times
+ * the plan currently in force for (M, N, K) -- pinned or the heuristic's -- and the heuristic's
+ * next best-scored plans, `top` in all (0 = 8, at most 64), on the caller's device A (M x K,
+ * lda) and B (K x N, ldb) writing a library scratch C (cudaMalloc'd and freed inside; alpha = 1,
+ * beta = 0), each as batches of back-to-back launches (>= ~2 ms, best of 3) timed with CUDA
+ * events on `cuda_stream`.  The fastest (ties within 0.3 % go to the plan in force, then to
+ * the better model score) is pinned as by gemm_plan_set and written to *cfg_id / *splits, its
+ * device seconds per call to *seconds (may be NULL).  Synchronous; A and B are only read.
+ * Candidates: the plan in force, each of the `top` best-scored configurations at its
+ * best-scored slice count, and slice counts S - 1, S + 1, 2S of the three best-scored ones;
+ * each costs about 5 calls of the shape.  Operands that miss the TMA rules are not timed (the
+ * heuristic's plan is returned, *seconds = 0).  Results of the pinned plan are within the
+ * documented bound like every plan; different plans may round differently.
+ * Errors: M, N or K <= 0, NULL pointers, top out of range -> GEMM_ERR_ARG; called while
+ * `cuda_stream` is capturing -> GEMM_ERR_UNSUPPORTED; scratch allocation -> GEMM_ERR_ALLOC;
+ * launch failures -> GEMM_ERR_CUDA (nothing pinned).
+ * With the environment variable GEMM_AUTOTUNE=1 (read once per process) the heuristic entry
+ * points (gemm_f64, gemm_f64_stream, gemm_f64_cfg / _ex with cfg_id = -1 and splits = 0) call
+ * this themselves, on the caller's stream, the first time they see a TMA shape that no table
+ * pins (that first call is then synchronous; skipped while capturing; attempted once per
+ * shape); gemm_tune_save persists the result for gemm_tune_load in later processes. */
+GEMM_API int gemm_plan_autotune(int64_t M, int64_t N, int64_t K, const double *A, int64_t lda,
+                       const double *B, int64_t ldb, int top, int *cfg_id, int *splits,
+                       double *seconds, void *cuda_stream);
 
 /* Thread-local message for the last non-OK return on this thread. */
 GEMM_API const char *gemm_last_error(void);
@@ -245,7 +274,9 @@ GEMM_API int gemm_comm_unique_id(unsigned char id_out[128]);
 /* Creates the library-owned communicator for `rank` of `nranks` on the current device
  * (collective over the nranks processes).  *comm_out receives an opaque handle owned by the
  * library (a private NCCL communicator, a communication stream, events and the column-panel
- * workspace), released by gemm_comm_destroy.  Bad rank / nranks / NULL -> GEMM_ERR_ARG;
+ * workspace), released by gemm_comm_destroy.  The environment variable GEMM_NCCL_MAX_CTAS (> 0)
+ * sets the communicator's maxCTAs, i.e. caps the SMs a panel broadcast running beside the
+ * GEMM (bcast_chunks > 1) can take; unset, NCCL chooses.  Bad rank / nranks / NULL -> GEMM_ERR_ARG;
  * NCCL failure -> GEMM_ERR_NCCL (nothing is left allocated). */
 GEMM_API int gemm_comm_init(void **comm_out, int nranks, const unsigned char id[128], int rank);
 /* Destroys a communicator (NULL is a no-op).  Collective like ncclCommDestroy; the caller

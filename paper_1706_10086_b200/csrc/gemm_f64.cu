@@ -421,14 +421,15 @@ static Choice choose(int64_t M, int64_t N, int64_t K, bool tma, bool single_pass
     return c;
 }
 
-static Choice choose_uncached(int64_t M, int64_t N, int64_t K, bool tma, bool single_pass) {
-    Choice best;
-    if (!tma) {
-        const int64_t tiles128 = ((M + 127) / 128) * ((N + 127) / 128);
-        best.id = find_cfg(tiles128 >= 2 * 148 ? "gen_128x128x16_w64x32_s4" : "gen_64x64x16_w32x16_s4");
-        return best;
-    }
-    double best_t = 1e300;
+// Model time of every TMA candidate plan for this shape, in candidate order (the order the
+// selection below scans; gemm_plan_autotune ranks them by t).
+struct Scored {
+    double t;
+    int id;
+    int splits;
+};
+
+static void score_all(int64_t M, int64_t N, int64_t K, bool single_pass, std::vector<Scored> &out) {
     const int sms = num_sms();
     for (const Cand &c : k_tma_cands) {
         const int id = find_cfg(c.name);
@@ -456,12 +457,7 @@ static Choice choose_uncached(int64_t M, int64_t N, int64_t K, bool tma, bool si
                 const int64_t gsk = std::min<int64_t>(G, std::max<int64_t>(tail, tail * KT / 16));
                 ks += ((double)((tail * KT + gsk - 1) / gsk) + 12.0 * u) / (c.eff_tail > 0 ? c.eff_tail : c.eff);
             }
-            const double t = ks * occ * d.bm * d.bn * (d.bk / 16.0);
-            if (t < best_t * 0.999) {
-                best_t = t;
-                best.id = id;
-                best.splits = 1;
-            }
+            out.push_back({ks * occ * d.bm * d.bn * (d.bk / 16.0), id, 1});
             continue;
         }
         if (d.split_k == -1) {   // stream-K: every CTA gets ceil(U/G) k-steps, no partial waves
@@ -475,24 +471,31 @@ static Choice choose_uncached(int64_t M, int64_t N, int64_t K, bool tma, bool si
             const double t = ((double)((tiles * KT + G - 1) / G) + (4.0 * per_cta_tiles + 6.0) * 16.0 / d.bk) * occ *
                              d.bm * d.bn *
                              (d.bk / 16.0) / c.eff;
-            if (t < best_t * 0.999) {
-                best_t = t;
-                best.id = id;
-                best.splits = 1;
-            }
+            out.push_back({t, id, 1});
             continue;
         }
         const int64_t scap = d.split_k == -3 ? 8 : 16;   // cluster split-K: portable cluster size
         const int smax = (d.split_k == 1 || single_pass) ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(scap, KT / 2));
-        for (int S = 1; S <= smax; ++S) {
-            const double t = est_time(d, occ, sms, M, N, K, S, c.eff);
-            if (t < best_t * 0.999) {
-                best_t = t;
-                best.id = id;
-                best.splits = S;
-            }
-        }
+        for (int S = 1; S <= smax; ++S) out.push_back({est_time(d, occ, sms, M, N, K, S, c.eff), id, S});
     }
+}
+
+static Choice choose_uncached(int64_t M, int64_t N, int64_t K, bool tma, bool single_pass) {
+    Choice best;
+    if (!tma) {
+        const int64_t tiles128 = ((M + 127) / 128) * ((N + 127) / 128);
+        best.id = find_cfg(tiles128 >= 2 * 148 ? "gen_128x128x16_w64x32_s4" : "gen_64x64x16_w32x16_s4");
+        return best;
+    }
+    std::vector<Scored> v;
+    score_all(M, N, K, single_pass, v);
+    double best_t = 1e300;
+    for (const Scored &c : v)   // first candidate more than 0.1 % faster than the best so far wins
+        if (c.t < best_t * 0.999) {
+            best_t = c.t;
+            best.id = c.id;
+            best.splits = c.splits;
+        }
     if (best.id < 0) best.id = 0;
     return best;
 }
@@ -707,6 +710,21 @@ static int raster_group(const gemm_cfg_desc &, int, int64_t M) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(g, M));
 }
 
+// GEMM_AUTOTUNE=1 (read once): the first heuristic call of a TMA shape that no table pins runs
+// gemm_plan_autotune on it (synchronously, on the caller's stream; skipped while capturing), so
+// later calls launch the measured-fastest plan.  Each shape is attempted once per process.
+static bool autotune_on_first_use(int64_t M, int64_t N, int64_t K) {
+    static const bool on = [] {
+        const char *e = std::getenv("GEMM_AUTOTUNE");
+        return e && std::atoi(e) > 0;
+    }();
+    if (!on) return false;
+    static std::set<std::tuple<int64_t, int64_t, int64_t>> attempted;
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    if (g_pinned.count(PlanKey{0, M, N, K, true})) return false;
+    return attempted.insert(std::make_tuple(M, N, K)).second;
+}
+
 int gemm_impl(int64_t M, int64_t N, int64_t K, double alpha, const double *A, int64_t lda, const double *B,
               int64_t ldb, double beta, double *C, int64_t ldc, int cfg_id, cudaStream_t st, int force_splits) {
     clear_error();
@@ -772,6 +790,12 @@ int gemm_impl(int64_t M, int64_t N, int64_t K, double alpha, const double *A, in
                              "(16-byte aligned, even lda/ldb)", force_splits);
         splits = force_splits;
     } else if (id < 0) {
+        if (force_splits == 0 && tma && autotune_on_first_use(M, N, K)) {
+            int acfg = 0, asp = 0;
+            rc = gemm_plan_autotune(M, N, K, A, lda, B, ldb, 0, &acfg, &asp, nullptr, st);
+            if (rc == GEMM_ERR_CUDA) return rc;
+            clear_error();   // no scratch memory / capturing: the model's plan below
+        }
         const Choice c = choose(M, N, K, tma, force_splits == 1);   // 1: one k-pass per tile
         id = c.id;
         splits = force_splits == 1 ? 1 : c.splits;
@@ -913,6 +937,31 @@ int gemm_tune_load(const char *path, int *n_loaded) {
     return GEMM_OK;
 }
 
+int gemm_tune_save(const char *path, int *n_saved) {
+    clear_error();
+    if (n_saved) *n_saved = 0;
+    if (!path) return set_error(GEMM_ERR_ARG, "path is NULL");
+    std::map<PlanKey, Choice> snap;
+    {
+        std::lock_guard<std::mutex> lk(g_plan_mu);
+        snap = g_pinned;
+    }
+    FILE *f = fopen(path, "w");
+    if (!f) return set_error(GEMM_ERR_ARG, "cannot write tuning table %s", path);
+    int n = 0;
+    bool ok = fprintf(f, "# M N K tma cfg_name splits (gemm_tune_save: %s)\n", gemm_version()) > 0;
+    for (const auto &kv : snap) {
+        ok = ok && fprintf(f, "%lld %lld %lld %d %s %d\n", (long long)kv.first.M, (long long)kv.first.N,
+                           (long long)kv.first.K, kv.first.tma ? 1 : 0, g_cfgs[kv.second.id].name,
+                           kv.second.splits) > 0;
+        ++n;
+    }
+    ok = (fclose(f) == 0) && ok;
+    if (!ok) return set_error(GEMM_ERR_ARG, "write to %s failed", path);
+    if (n_saved) *n_saved = n;
+    return GEMM_OK;
+}
+
 int gemm_plan(int64_t M, int64_t N, int64_t K, const double *A, int64_t lda, const double *B, int64_t ldb,
               int *cfg_id, int *splits) {
     clear_error();
@@ -934,6 +983,119 @@ int gemm_plan_ex(int64_t M, int64_t N, int64_t K, const double *A, int64_t lda, 
     const Choice c = choose(M, N, K, tma_ok(A, lda, B, ldb), one_pass != 0);
     *cfg_id = c.id;
     *splits = one_pass ? 1 : c.splits;
+    return GEMM_OK;
+}
+
+// One-time timed choice among the model's best-scored plans (the paper's "tuning ... for each
+// architecture", §2.3, done for one shape at run time, like the offline tuner.py):
+// the plan in force (pinned or model) first, then the other candidates by model time; each runs
+// on the caller's A and B into a library scratch C (alpha = 1, beta = 0) and is timed with
+// events on `stream`; the fastest (ties within 0.3 % go to the earlier one) is pinned.
+int gemm_plan_autotune(int64_t M, int64_t N, int64_t K, const double *A, int64_t lda, const double *B,
+                       int64_t ldb, int top, int *cfg_id, int *splits, double *seconds, void *stream) {
+    clear_error();
+    if (!cfg_id || !splits) return set_error(GEMM_ERR_ARG, "cfg_id / splits is NULL");
+    if (M <= 0 || N <= 0 || K <= 0) return set_error(GEMM_ERR_ARG, "autotune needs M, N, K > 0");
+    if (!A || !B) return set_error(GEMM_ERR_ARG, "A / B is NULL");
+    if (top < 0 || top > 64) return set_error(GEMM_ERR_ARG, "top=%d not in [0, 64]", top);
+    if (top == 0) top = 8;
+    const cudaStream_t st = (cudaStream_t)stream;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    int rc = cuda_check(cudaStreamIsCapturing(st, &cap), "cudaStreamIsCapturing");
+    if (rc) return rc;
+    if (cap != cudaStreamCaptureStatusNone)
+        return set_error(GEMM_ERR_UNSUPPORTED, "gemm_plan_autotune synchronizes: not allowed while capturing");
+    const int64_t elda = lda + (M == 1 ? (lda & 1) : 0), eldb = ldb + (K == 1 ? (ldb & 1) : 0);
+    const bool tma = tma_ok(A, elda, B, eldb);
+    const Choice cur = choose(M, N, K, tma);
+    *cfg_id = cur.id;
+    *splits = cur.splits;
+    if (seconds) *seconds = 0.0;
+    if (!tma) return GEMM_OK;   // cp.async operands: one configuration per size class, nothing to time
+
+    // candidates: the plan in force; each of the `top` best-scored configurations at its
+    // best-scored slice count; the neighbouring slice counts (S - 1, S + 1, 2S) of the three
+    // best-scored configurations (the model ranks configurations better than slice counts:
+    // profiles/r02/regret_small_seed29_auto8.csv)
+    std::vector<Choice> cands{cur};
+    {
+        std::vector<Scored> v;
+        score_all(M, N, K, false, v);
+        std::vector<Scored> per_cfg;
+        for (const Scored &x : v) {
+            auto it = std::find_if(per_cfg.begin(), per_cfg.end(), [&](const Scored &e) { return e.id == x.id; });
+            if (it == per_cfg.end())
+                per_cfg.push_back(x);
+            else if (x.t < it->t)
+                *it = x;
+        }
+        std::stable_sort(per_cfg.begin(), per_cfg.end(), [](const Scored &a, const Scored &b) { return a.t < b.t; });
+        auto add = [&](int id, int S) {
+            for (const Choice &c : cands)
+                if (c.id == id && c.splits == S) return;
+            cands.push_back(Choice{id, S});
+        };
+        for (size_t i = 0; i < per_cfg.size() && (int)i < top; ++i) add(per_cfg[i].id, per_cfg[i].splits);
+        for (size_t i = 0; i < per_cfg.size() && i < 3; ++i)
+            for (int S : {per_cfg[i].splits - 1, per_cfg[i].splits + 1, 2 * per_cfg[i].splits})
+                for (const Scored &x : v)
+                    if (x.id == per_cfg[i].id && x.splits == S) add(x.id, S);
+    }
+    double *Cs = nullptr;
+    if (cudaMalloc(&Cs, (size_t)M * (size_t)N * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(GEMM_ERR_ALLOC, "scratch C of %lld x %lld doubles", (long long)M, (long long)N);
+    }
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    auto run = [&](const Choice &c) {
+        return gemm_impl(M, N, K, 1.0, A, lda, B, ldb, 0.0, Cs, N, c.id, st, c.splits);
+    };
+    auto timed = [&](const Choice &c, int n, double *sec) {
+        int r = cuda_check(cudaEventRecord(e0, st), "cudaEventRecord");
+        for (int i = 0; i < n && !r; ++i) r = run(c);
+        if (!r) r = cuda_check(cudaEventRecord(e1, st), "cudaEventRecord");
+        if (!r) r = cuda_check(cudaEventSynchronize(e1), "cudaEventSynchronize");
+        float ms = 0.f;
+        if (!r) r = cuda_check(cudaEventElapsedTime(&ms, e0, e1), "cudaEventElapsedTime");
+        *sec = 1e-3 * ms / n;
+        return r;
+    };
+    std::vector<double> t(cands.size(), 1e300);
+    rc = GEMM_OK;
+    for (size_t i = 0; i < cands.size() && !rc; ++i) {
+        int r = run(cands[i]);   // warm-up: plan, workspace, tensor maps
+        if (r == GEMM_ERR_UNSUPPORTED || r == GEMM_ERR_ARG) {
+            if (i == 0) rc = r;   // the plan in force must run
+            clear_error();
+            continue;
+        }
+        double t1 = 0.0, tb = 0.0;
+        if (!r) r = timed(cands[i], 1, &t1);
+        // batches of back-to-back calls (>= ~2 ms) so host launch cost overlaps the kernels
+        const int n = (int)std::max(1.0, std::min(256.0, std::ceil(2e-3 / std::max(t1, 1e-7))));
+        for (int rep = 0; rep < 3 && !r; ++rep) {
+            r = timed(cands[i], n, &tb);
+            t[i] = std::min(t[i], tb);
+        }
+        rc = r;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamSynchronize(st);
+    cudaFree(Cs);
+    if (rc) return rc;
+    const double tmin = *std::min_element(t.begin(), t.end());
+    size_t pick = 0;
+    while (t[pick] > tmin * 1.003) ++pick;
+    {
+        std::lock_guard<std::mutex> lk(g_plan_mu);
+        g_pinned[PlanKey{0, M, N, K, true}] = cands[pick];
+    }
+    *cfg_id = cands[pick].id;
+    *splits = cands[pick].splits;
+    if (seconds) *seconds = t[pick];
     return GEMM_OK;
 }
 

@@ -17,6 +17,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "../../include/gemm_f64.h"
@@ -83,6 +84,12 @@ int gemm_comm_init(void **comm_out, int nranks, const unsigned char id[128], int
         for (int i = 0; i < 128; ++i) uid.internal[i] = (char)id[i];
         ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
         cfg.blocking = 1;
+        // GEMM_NCCL_MAX_CTAS caps the CTAs NCCL's kernels take (the SMs a concurrent panel
+        // broadcast steals from the GEMM with bcast_chunks > 1); unset = NCCL's default
+        if (const char *e = std::getenv("GEMM_NCCL_MAX_CTAS")) {
+            const int v = std::atoi(e);
+            if (v > 0) cfg.maxCTAs = v;
+        }
         rc = nccl_check(ncclCommInitRankConfig(&c->nccl, nranks, uid, rank, &cfg), "ncclCommInitRankConfig");
     }
     if (rc) {

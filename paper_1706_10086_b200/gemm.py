@@ -26,7 +26,7 @@ EXPORTS = ("gemm_f64", "gemm_f64_stream", "gemm_f64_cfg", "gemm_f64_ex", "gemm_f
            "gemm_f32_cfg", "gemm_f32_num_cfgs", "gemm_f32_cfg_name", "gemm_f64_host", "gemm_host_pool_release",
            "gemm_workspace_release",
            "gemm_num_cfgs", "gemm_cfg_name", "gemm_cfg_info", "gemm_cfg_select", "gemm_plan", "gemm_plan_ex", "gemm_plan_set",
-           "gemm_plan_clear", "gemm_tune_load", "gemm_last_error",
+           "gemm_plan_clear", "gemm_tune_load", "gemm_tune_save", "gemm_plan_autotune", "gemm_last_error",
            "gemm_fill_f64", "gemm_peak_probe", "gemm_comm_unique_id", "gemm_comm_init",
            "gemm_comm_destroy", "gemm_comm_info", "gemm_f64_sharded", "gemm_bcast_f64", "gemm_version")
 
@@ -71,6 +71,9 @@ def _load():
         "gemm_plan_set": (ci, [i64, i64, i64, ci, ci, ci]),
         "gemm_plan_clear": (ci, []),
         "gemm_tune_load": (ci, [ctypes.c_char_p, ctypes.POINTER(ci)]),
+        "gemm_tune_save": (ci, [ctypes.c_char_p, ctypes.POINTER(ci)]),
+        "gemm_plan_autotune": (ci, [i64, i64, i64, vp, i64, vp, i64, ci, ctypes.POINTER(ci), ctypes.POINTER(ci),
+                                    ctypes.POINTER(dbl), vp]),
         "gemm_last_error": (ctypes.c_char_p, []),
         "gemm_fill_f64": (ci, [ci, ctypes.c_uint64, ci, i64, i64, i64, i64, vp, i64, vp]),
         "gemm_peak_probe": (ci, [ci, ci, ci, i64, vp, vp, vp]),
@@ -388,10 +391,31 @@ def plan_clear():
     _check(_lib.gemm_plan_clear())
 
 
+def autotune(A, B, top: int = 0, stream=None) -> tuple:
+    """Time the plan in force and the heuristic's next best plans for A @ B's shape on these
+    operands and pin the fastest (gemm_plan_autotune).  Returns (cfg_id, splits, seconds)."""
+    pa, M, K, lda = _mat(A, "A")
+    pb, K2, N, ldb = _mat(B, "B")
+    if K != K2:
+        raise ValueError(f"inner dimensions differ: A is {M}x{K}, B is {K2}x{N}")
+    _on_current_device(A, B, names="AB")
+    cid, sp, sec = ctypes.c_int(), ctypes.c_int(), ctypes.c_double()
+    _check(_lib.gemm_plan_autotune(M, N, K, pa, lda, pb, ldb, int(top), ctypes.byref(cid), ctypes.byref(sp),
+                                   ctypes.byref(sec), _stream_ptr(stream)))
+    return cid.value, sp.value, sec.value
+
+
 def tune_load(path: str) -> int:
     """Load a persisted tuning table (lines "M N K tma cfg_name splits"); returns entries loaded."""
     n = ctypes.c_int()
     _check(_lib.gemm_tune_load(os.fsencode(path), ctypes.byref(n)))
+    return n.value
+
+
+def tune_save(path: str) -> int:
+    """Write every pinned plan (table, plan_set, autotune) in tune_load's format; returns lines written."""
+    n = ctypes.c_int()
+    _check(_lib.gemm_tune_save(os.fsencode(path), ctypes.byref(n)))
     return n.value
 
 

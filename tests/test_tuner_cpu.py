@@ -58,3 +58,35 @@ def test_table_errors(T, tmp_path):
         G.plan_set(4, 4, 4, True, G.cfg_id("tma_128x128x16_w32x32_s4"), 2)   # no split-K on this cfg
     with pytest.raises(G.GemmError):
         G.plan_set(4, 4, 4, False, G.cfg_id("tma_128x128x16_w32x32_s4"), 1)  # TMA cfg for a non-TMA shape
+
+
+def test_tune_save_round_trip(T, tmp_path):
+    """gemm_tune_save writes every pinned plan in gemm_tune_load's format: the shipped table
+    saved and re-read pins the same (M, N, K, tma) -> (cfg, splits) map."""
+    from paper_1706_10086_b200 import gemm as G
+
+    def parse(path):
+        out = {}
+        for line in open(path):
+            if line.startswith("#") or not line.strip():
+                continue
+            M, N, K, tma, name, sp = line.split()
+            out[(int(M), int(N), int(K), int(tma))] = (name, int(sp))
+        return out
+
+    G.plan_clear()
+    n = G.tune_load(G.TUNED_TABLE)
+    path = str(tmp_path / "saved.txt")
+    assert G.tune_save(path) == n == len(parse(G.TUNED_TABLE))
+    assert parse(path) == parse(G.TUNED_TABLE)
+    G.plan_clear()
+    assert G.tune_save(path) == 0 and parse(path) == {}
+    G.plan_set(777, 555, 333, True, G.cfg_id("tma_64x64x16_w32x16_s6_splitk"), 3)
+    assert G.tune_save(path) == 1
+    G.plan_clear()
+    assert G.tune_load(path) == 1
+    assert G.plan(777, 555, 333, 0, 334, 0, 556) == (G.cfg_id("tma_64x64x16_w32x16_s6_splitk"), 3)
+    with pytest.raises(G.GemmError, match="cannot write"):
+        G.tune_save(str(tmp_path / "no_such_dir" / "t.txt"))
+    G.plan_clear()
+    G.tune_load(G.TUNED_TABLE)

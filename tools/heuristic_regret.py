@@ -1,7 +1,8 @@
 """How good is the size heuristic on shapes it was not tuned on?  For seeded random shapes
 (and a few skinny ones) time the product's own plan and every tuner candidate (batched
 back-to-back timing, paper_1706_10086_b200.tuner), and report the plan's regret
-t_plan / t_best - 1.  Shapes in the tuned table are skipped (they are pinned).
+t_plan / t_best - 1, and
+with --autotune also the plan gemm_plan_autotune pins (timed the same way) and its regret.  Shapes in the tuned table are skipped (they are pinned).
 
     python tools/heuristic_regret.py [--n 16] [--seed 7] [--out gpurun_out/regret.csv]
 """
@@ -35,10 +36,12 @@ def main():
     ap.add_argument("--out", default="gpurun_out/regret.csv")
     ap.add_argument("--lo", type=int, default=500, help="shape range (small shapes: --lo 200 --hi 1600)")
     ap.add_argument("--hi", type=int, default=6000)
+    ap.add_argument("--autotune", type=int, default=0, help="also run gemm_plan_autotune with this top (0: off)")
     a = ap.parse_args()
     with open(a.out, "w", newline="") as f:
         w = csv.writer(f)
-        w.writerow(["m", "n", "k", "plan", "plan_splits", "plan_tflops", "best", "best_splits", "best_tflops", "regret"])
+        w.writerow(["m", "n", "k", "plan", "plan_splits", "plan_tflops", "best", "best_splits", "best_tflops", "regret"]
+                   + (["auto", "auto_splits", "auto_tflops", "auto_regret", "autotune_s"] if a.autotune else []))
         for (M, N, K) in shapes(a.n, a.seed, a.lo, a.hi):
             Ke, Ne = K + (K & 1), N + (N & 1)        # even leading dimensions: the TMA path
             A = torch.empty((M, Ke), dtype=torch.float64, device="cuda")[:, :K]
@@ -56,6 +59,14 @@ def main():
                     best = (cfg, s, t)
             r = [M, N, K, G.cfg_name(cid), sp, f"{fl / t_plan / 1e12:.3f}", G.cfg_name(best[0]), best[1],
                  f"{fl / best[2] / 1e12:.3f}", f"{t_plan / best[2] - 1.0:.4f}"]
+            if a.autotune:
+                torch.cuda.synchronize()
+                import time
+                w0 = time.perf_counter()
+                acid, asp, _ = G.autotune(A, B, top=a.autotune)
+                wall = time.perf_counter() - w0
+                t_auto, _ = tuner._time(lambda: G.gemm(A, B, C, 1.0, 0.0), 5)
+                r += [G.cfg_name(acid), asp, f"{fl / t_auto / 1e12:.3f}", f"{t_auto / best[2] - 1.0:.4f}", f"{wall:.3f}"]
             w.writerow(r)
             f.flush()
             print(",".join(map(str, r)), flush=True)
