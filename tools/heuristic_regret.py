@@ -37,6 +37,7 @@ def main():
     ap.add_argument("--lo", type=int, default=500, help="shape range (small shapes: --lo 200 --hi 1600)")
     ap.add_argument("--hi", type=int, default=6000)
     ap.add_argument("--autotune", type=int, default=0, help="also run gemm_plan_autotune with this top (0: off)")
+    ap.add_argument("--dump", default=None, help="JSONL of every candidate's seconds per shape (model fitting)")
     a = ap.parse_args()
     with open(a.out, "w", newline="") as f:
         w = csv.writer(f)
@@ -53,10 +54,17 @@ def main():
             fl = 2.0 * M * N * K
             t_plan, _ = tuner._time(lambda: G.gemm(A, B, C, 1.0, 0.0), 5)
             best = (None, None, float("inf"))
+            times = {}
             for cfg, s in tuner.candidates(M, N, K):
                 t, _ = tuner._time(lambda: G.gemm(A, B, C, 1.0, 0.0, cfg=cfg, splits=s), 3, warm_s=0.05)
+                times[f"{G.cfg_name(cfg)}:{s}"] = t
                 if t < best[2]:
                     best = (cfg, s, t)
+            if a.dump:
+                import json
+                with open(a.dump, "a") as df:
+                    df.write(json.dumps({"shape": [M, N, K], "plan": f"{G.cfg_name(cid)}:{sp}", "plan_s": t_plan,
+                                         "times": times}) + "\n")
             r = [M, N, K, G.cfg_name(cid), sp, f"{fl / t_plan / 1e12:.3f}", G.cfg_name(best[0]), best[1],
                  f"{fl / best[2] / 1e12:.3f}", f"{t_plan / best[2] - 1.0:.4f}"]
             if a.autotune:
@@ -76,3 +84,8 @@ def main():
 
 if __name__ == "__main__":
     main()
+    if "--dump" in sys.argv:   # per-configuration registers / smem / threads after use (occupancy)
+        import json
+        p = sys.argv[sys.argv.index("--dump") + 1]
+        with open(p, "a") as df:
+            df.write(json.dumps({"cfgs": [G.cfg_info(i) | {"name": G.cfg_name(i)} for i in range(G.num_cfgs())]}) + "\n")
