@@ -50,7 +50,7 @@ def est_time(d, occ, sms, M, N, K, S, eff):
                 c = occ
             units += c if c >= 2 else 1.0 / 0.6
     u = 16.0 / d["bk"]
-    ksteps = -(-KT // S) + (4.0 + (2.0 if S > 1 else 0.0)) * u
+    ksteps = -(-KT // S) + 2.0 * u     # model v4 (was 4 + 2 for a split)
     return units * d["bm"] * d["bn"] * ksteps * (d["bk"] / 16.0) / eff
 
 
