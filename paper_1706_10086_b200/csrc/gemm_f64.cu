@@ -335,10 +335,14 @@ static const Cand k_tma_cands[] = {
     // One CTA per SM (32x64x64, 144 KB) runs at a lone 8-warp CTA's ~0.95 (lone_cta_rate_v1.jsonl);
     // 32x32 tiles move twice the shared-memory bytes per FLOP and a 2-stage ring hides less
     // latency on long k-ranges (charged 0.90 / 0.96: measured to lose mid shapes with more,
-    // profiles/r02/regret_seed23_m2.csv)
-    {"tma_32x64x32_w16x16_s3_splitk", 0.985},  {"tma_32x64x64_w16x16_s3_splitk", 0.950},
-    {"tma_64x32x32_w16x16_s4_splitk", 0.980},  {"tma_32x32x32_w16x16_s4_splitk", 0.900},
-    {"tma_32x64x32_w16x16_s3_splitk_mb3", 0.985}, {"tma_32x64x32_w16x16_s2_splitk_mb3", 0.960},
+    // profiles/r02/regret_seed23_m2.csv).  Model v4: the E = 8 efficiencies below and the fixed
+    // cost in est_time were fitted to every candidate's measured time on 65 unseen shapes
+    // (tools/model_fit_search.py on profiles/r02/dump_*.jsonl; mean regret small 6.3-7.6 % ->
+    // 2.4-4.6 %, mid 1.5 -> 0.75 %); 64x32 keeps its steady-state 0.98 (a higher value fits the
+    // small shapes but would send large ones to it)
+    {"tma_32x64x32_w16x16_s3_splitk", 0.837},  {"tma_32x64x64_w16x16_s3_splitk", 0.807},
+    {"tma_64x32x32_w16x16_s4_splitk", 0.980},  {"tma_32x32x32_w16x16_s4_splitk", 0.810},
+    {"tma_32x64x32_w16x16_s3_splitk_mb3", 0.970}, {"tma_32x64x32_w16x16_s2_splitk_mb3", 0.960},
 };
 
 struct Choice {
@@ -374,9 +378,11 @@ static double est_time(const gemm_cfg_desc &d, int occ, int sms, int64_t M, int6
         }
     }
     // fixed costs are counted in 16-deep k-steps (pipeline fill, epilogue, split reduction),
-    // so a BK = 32 stage is charged half as many of its own steps
+    // so a BK = 32 stage is charged half as many of its own steps.  Model v4: 2 k-steps, none
+    // extra for the split reduction (was 4 + 2; fitted, see the E = 8 candidates above -- the
+    // slice-ordered finish overlaps the reduction with the other slices' main loops)
     const double u = 16.0 / d.bk;
-    const double ksteps = (double)((KT + S - 1) / S) + (4.0 + (S > 1 ? 2.0 : 0.0)) * u;
+    const double ksteps = (double)((KT + S - 1) / S) + 2.0 * u;
     return units * d.bm * d.bn * ksteps * (d.bk / 16.0) / eff;
 }
 

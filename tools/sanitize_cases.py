@@ -57,8 +57,16 @@ def main():
     hA, hB = np.random.rand(300, 200), np.random.rand(200, 100)
     hC = np.zeros((300, 100))
     G.gemm_host(hA, hB, hC, 1.0, 0.0)
+    # run-time tuning: candidates into the library's scratch C, then the pinned plan
+    M, N, K = 222, 350, 410
+    A = torch.rand((M, K), dtype=torch.float64, device="cuda")
+    B = torch.rand((K, N), dtype=torch.float64, device="cuda")
+    C = torch.zeros((M, N), dtype=torch.float64, device="cuda")
+    G.autotune(A, B, top=4)
+    G.gemm(A, B, C, 1.0, 0.0)
+    n += 1
     torch.cuda.synchronize()
-    print(f"sanitize cases ok: {n + 2} calls")
+    print(f"sanitize cases ok: {n + 2} calls (+ one autotune)")
 
 
 if __name__ == "__main__":
