@@ -223,14 +223,23 @@ def run_reference(a):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * tot / a.steps, "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": wname, "M": M, "N": N, "K": K, "alpha": 1.0, "beta": 0.0,
-                       "sample_rows_per_step": R, "parallelism": "host threads"},
+            "config": workload_config(wname, M, N, K, world),
+            "impl_detail": {"sample_rows_per_step": R, "parallelism": f"{threads} host threads",
+                            "inputs": "synth generator (host)"},
             "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
                              "sample": f"{R} rows of the {M}x{N}x{K} problem per step (i-k-j C oracle)",
                              "cpu_model": cpu_model(), "table": CPU_TABLE},
             "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def workload_config(wname, M, N, K, world):
+    """The `config` both arms print (the workload, identical for the GPU arm and the reference
+    arm at the same N); how each arm executes it goes to `impl_detail`."""
+    return {"workload": wname, "M": M, "N": N, "K": K, "rows_per_gpu": M // world, "alpha": 1.0, "beta": 0.0,
+            "inputs": "seeded uniform[-1,1) (synth counter-based generator, seed 1706)",
+            "l2": "inputs larger than L2 (no flush)"}
 
 
 # ---------------------------------------------------------------------- parity (post-timing)
@@ -590,11 +599,10 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": a.steps,
                 "warmup": a.warmup, "ms_per_step": t_ms / a.steps, "higher_is_better": True, "scaling": scaling,
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": wname, "M": M, "N": N, "K": K, "rows_per_gpu": Ml, "alpha": 1.0,
-                           "beta": 0.0, "inputs": "seeded uniform[-1,1) (synth generator, device fill)",
-                           "l2": "inputs larger than L2 (no flush)", "kernel_cfg": cfg_name,
-                           "parallelism": f"row-sharded x{world}, B broadcast (NCCL)" if world > 1 else "1 GPU",
-                           "step": step_via},
+                "config": workload_config(wname, M, N, K, world),
+                "impl_detail": {"kernel_cfg": cfg_name, "inputs": "synth generator's device twin (gemm_fill_f64)",
+                                "parallelism": f"row-sharded x{world}, B broadcast (NCCL)" if world > 1 else "1 GPU",
+                                "step": step_via},
                 "pct_of_fp64_peak": 100.0 * value / (FP64_DATASHEET_TFLOPS * world),
                 "clocks": clocks, "roofline": roofline, "parity": parity, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": a.steps * launches_per_step}

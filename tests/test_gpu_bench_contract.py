@@ -35,6 +35,6 @@ def test_bench_json_line_contract(cuda_lib):
     # every rank checked its own result after the timed region
     assert d["parity"]["ok"] is True and d["parity"]["b_bitwise"] is True
     assert d["parity"]["rows_checked_total"] >= 2 and d["parity"]["max_ratio"] < 0.05
-    assert r["kernel"] == d["config"]["kernel_cfg"]
+    assert r["kernel"] == d["impl_detail"]["kernel_cfg"]
     assert d["gpu_launches"] == 3 * r["launches_per_gemm"] >= 3
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
