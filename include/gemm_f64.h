@@ -219,10 +219,13 @@ GEMM_API int gemm_tune_save(const char *path, int *n_saved);
  * device seconds per call to *seconds (may be NULL).  Synchronous; A and B are only read.
  * Candidates: the plan in force, each of the `top` best-scored configurations at its
  * best-scored slice count, and slice counts S - 1, S + 1, 2S of the three best-scored ones;
- * each costs about 5 calls of the shape.  Operands that miss the TMA rules are not timed (the
- * heuristic's plan is returned, *seconds = 0).  Results of the pinned plan are within the
+ * each costs about 5 calls of the shape.  Operands that miss the TMA rules (alignment, odd
+ * leading dimension) are timed on packed copies when the problem is large enough for the
+ * heuristic call to repack them (2MNK >= 4e9, M, N >= 64, K >= 16), which then launches the
+ * pinned plan; smaller ones run their size class's cp.async configuration and are not timed
+ * (the heuristic's plan is returned, *seconds = 0).  Results of the pinned plan are within the
  * documented bound like every plan; different plans may round differently.
- * Errors: M, N or K <= 0, NULL pointers, top out of range -> GEMM_ERR_ARG; called while
+ * Errors: M, N or K <= 0, NULL pointers, lda < K, ldb < N, top out of range -> GEMM_ERR_ARG; called while
  * `cuda_stream` is capturing -> GEMM_ERR_UNSUPPORTED; scratch allocation -> GEMM_ERR_ALLOC;
  * launch failures -> GEMM_ERR_CUDA (nothing pinned).
  * With the environment variable GEMM_AUTOTUNE=1 (read once per process) the heuristic entry

@@ -716,6 +716,11 @@ static int raster_group(const gemm_cfg_desc &, int, int64_t M) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(g, M));
 }
 
+// Heuristic calls on operands that miss the TMA rules repack them when the problem is this large.
+static bool repack_eligible(int64_t M, int64_t N, int64_t K) {
+    return 2.0 * (double)M * (double)N * (double)K >= 4e9 && M >= 64 && N >= 64 && K >= 16;
+}
+
 // GEMM_AUTOTUNE=1 (read once): the first heuristic call of a TMA shape that no table pins runs
 // gemm_plan_autotune on it (synchronously, on the caller's stream; skipped while capturing), so
 // later calls launch the measured-fastest plan.  Each shape is attempted once per process.
@@ -757,7 +762,7 @@ int gemm_impl(int64_t M, int64_t N, int64_t K, double alpha, const double *A, in
     // O(MK + KN) bytes against O(MNK) flops) and take the TMA path; values and hence the
     // per-entry arithmetic are unchanged.  Small ones, or if the workspace cannot be had,
     // run the cp.async kernel.
-    if (!tma && cfg_id < 0 && 2.0 * (double)M * (double)N * (double)K >= 4e9 && M >= 64 && N >= 64 && K >= 16) {
+    if (!tma && cfg_id < 0 && repack_eligible(M, N, K)) {
         const double *pA = A, *pB = B;
         int64_t plda = lda, pldb = ldb;
         bool ok = true;
@@ -1003,6 +1008,7 @@ int gemm_plan_autotune(int64_t M, int64_t N, int64_t K, const double *A, int64_t
     if (!cfg_id || !splits) return set_error(GEMM_ERR_ARG, "cfg_id / splits is NULL");
     if (M <= 0 || N <= 0 || K <= 0) return set_error(GEMM_ERR_ARG, "autotune needs M, N, K > 0");
     if (!A || !B) return set_error(GEMM_ERR_ARG, "A / B is NULL");
+    if (lda < K || ldb < N) return set_error(GEMM_ERR_ARG, "lda=%lld < K or ldb=%lld < N", (long long)lda, (long long)ldb);
     if (top < 0 || top > 64) return set_error(GEMM_ERR_ARG, "top=%d not in [0, 64]", top);
     if (top == 0) top = 8;
     const cudaStream_t st = (cudaStream_t)stream;
@@ -1012,12 +1018,47 @@ int gemm_plan_autotune(int64_t M, int64_t N, int64_t K, const double *A, int64_t
     if (cap != cudaStreamCaptureStatusNone)
         return set_error(GEMM_ERR_UNSUPPORTED, "gemm_plan_autotune synchronizes: not allowed while capturing");
     const int64_t elda = lda + (M == 1 ? (lda & 1) : 0), eldb = ldb + (K == 1 ? (ldb & 1) : 0);
-    const bool tma = tma_ok(A, elda, B, eldb);
+    bool tma = tma_ok(A, elda, B, eldb);
+    if (seconds) *seconds = 0.0;
+    // operands that miss the TMA rules: gemm_impl repacks large ones into aligned rows and runs
+    // the TMA plan of (M, N, K), so that plan is tuned here on packed copies; small ones run the
+    // cp.async configuration of their size class and there is nothing to time
+    double *packed[2] = {nullptr, nullptr};
+    auto free_packed = [&] {
+        cudaStreamSynchronize(st);
+        for (double *p : packed)
+            if (p) cudaFree(p);
+    };
+    if (!tma && repack_eligible(M, N, K)) {
+        const int64_t plda = K + (K & 1), pldb = N + (N & 1);
+        if (cudaMalloc(&packed[0], (size_t)M * plda * sizeof(double)) != cudaSuccess ||
+            cudaMalloc(&packed[1], (size_t)K * pldb * sizeof(double)) != cudaSuccess) {
+            cudaGetLastError();
+            free_packed();
+            return set_error(GEMM_ERR_ALLOC, "autotune: packed copies of A / B");
+        }
+        rc = cuda_check(cudaMemcpy2DAsync(packed[0], plda * 8, A, lda * 8, K * 8, M, cudaMemcpyDeviceToDevice, st),
+                        "autotune: pack A");
+        if (!rc)
+            rc = cuda_check(cudaMemcpy2DAsync(packed[1], pldb * 8, B, ldb * 8, N * 8, K, cudaMemcpyDeviceToDevice, st),
+                            "autotune: pack B");
+        if (rc) {
+            free_packed();
+            return rc;
+        }
+        A = packed[0];
+        B = packed[1];
+        lda = plda;
+        ldb = pldb;
+        tma = tma_ok(A, lda, B, ldb);
+    }
     const Choice cur = choose(M, N, K, tma);
     *cfg_id = cur.id;
     *splits = cur.splits;
-    if (seconds) *seconds = 0.0;
-    if (!tma) return GEMM_OK;   // cp.async operands: one configuration per size class, nothing to time
+    if (!tma) {
+        free_packed();
+        return GEMM_OK;
+    }
 
     // candidates: the plan in force; each of the `top` best-scored configurations at its
     // best-scored slice count; the neighbouring slice counts (S - 1, S + 1, 2S) of the three
@@ -1050,6 +1091,7 @@ int gemm_plan_autotune(int64_t M, int64_t N, int64_t K, const double *A, int64_t
     double *Cs = nullptr;
     if (cudaMalloc(&Cs, (size_t)M * (size_t)N * sizeof(double)) != cudaSuccess) {
         cudaGetLastError();
+        free_packed();
         return set_error(GEMM_ERR_ALLOC, "scratch C of %lld x %lld doubles", (long long)M, (long long)N);
     }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -1091,6 +1133,7 @@ int gemm_plan_autotune(int64_t M, int64_t N, int64_t K, const double *A, int64_t
     cudaEventDestroy(e1);
     cudaStreamSynchronize(st);
     cudaFree(Cs);
+    free_packed();
     if (rc) return rc;
     const double tmin = *std::min_element(t.begin(), t.end());
     size_t pick = 0;

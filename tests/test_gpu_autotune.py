@@ -151,3 +151,31 @@ def test_env_autotune_on_first_use(cuda_lib, tmp_path):
     assert len(mine) == 1 and int(mine[0][3]) == 1
     assert cuda_lib.cfg_id(mine[0][4]) == int(r["after"][0]) and int(mine[0][5]) == int(r["after"][1])
     assert int(r["n"]) == len(lines)
+
+
+def test_autotune_repacked_operands(cuda_lib):
+    """Odd leading dimensions on a problem large enough to be repacked: autotune times the
+    TMA plan on packed copies and pins it under the TMA key, which the heuristic call (that
+    repacks) then launches -- bitwise equal to forcing that plan on aligned copies."""
+    G = cuda_lib
+    M, N, K = 1201, 1203, 1501                   # 2MNK = 4.3e9 >= the repack threshold
+    A, B, C0 = synth.problem(M, N, K, seed=77)
+    dA, dB = dev(A), dev(B)                      # packed: lda = 1501, ldb = 1203 (odd)
+    cid, sp, sec = G.autotune(dA, dB, top=4)
+    assert sec > 0.0 and G.cfg_info(cid)["tma"]
+    assert G.plan(M, N, K, 0, K + 1, 0, N + 1) == (cid, sp)
+    dC = dev(C0)
+    G.gemm(dA, dB, dC, 1.5, 0.5)
+    aA = torch.empty((M, K + 1), dtype=torch.float64, device="cuda")[:, :K]
+    aB = torch.empty((K, N + 1), dtype=torch.float64, device="cuda")[:, :N]
+    aA.copy_(dA)
+    aB.copy_(dB)
+    aC = torch.empty((M, N + 1), dtype=torch.float64, device="cuda")[:, :N]
+    aC.copy_(dev(C0))
+    G.gemm(aA, aB, aC, 1.5, 0.5, cfg=cid, splits=sp)
+    torch.cuda.synchronize()
+    assert torch.equal(dC, aC)
+    rows = [0, 1, 600, 1199, 1200]
+    ref, mag = oracle.dgemm(1.5, A[rows], B, 0.5, C0[rows], want_mag=True)
+    r = oracle.check(dC.cpu().numpy()[rows], ref, oracle.bound(K, 1.5, 0.5, mag, C0[rows]))
+    assert r.ok, str(r)

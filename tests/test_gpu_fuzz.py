@@ -56,3 +56,13 @@ def test_random_cases(cuda_lib, case):
     for i in range(M):
         mask[offs[2] + i * ldc: offs[2] + i * ldc + N] = False
     assert np.all(np.isnan(full[mask]))
+
+
+@pytest.mark.skipif(not os.environ.get("GEMM_AUTOTUNE"), reason="autotune soak only (GEMM_AUTOTUNE=1)")
+def test_autotune_soak_engaged(cuda_lib, tmp_path):
+    """Under GEMM_AUTOTUNE=1 the heuristic calls above tuned and pinned their shapes: more plans
+    are pinned than the shipped table holds."""
+    n_table = sum(1 for line in open(cuda_lib.TUNED_TABLE) if line.strip() and not line.startswith("#"))
+    n = cuda_lib.tune_save(str(tmp_path / "pinned.txt"))
+    print(f"pinned plans: {n} (table {n_table})")
+    assert n > n_table
