@@ -4,7 +4,7 @@ pinned), GEMM blocks timed with a wave model calibrated on the measured 16384^3 
 (240.8 ms: 111 waves of 256x64 tiles).  Used to choose the schedule geometry in
 csrc/host_api.cu; prints the old and the implemented schedule and the best of a grid.
 
-    python tools/e2e_sim.py [N]
+    python tools/e2e_sim.py [N] [--r02]
 """
 import math
 import sys
@@ -19,6 +19,16 @@ H2D, D2H = 55e9, 53e9
 def gemm_t(M, N, K):
     tiles = math.ceil(M / 256) * math.ceil(N / 64)
     return math.ceil(tiles / S) * (256 * 64 * K * 2 / RATE_SM + TILE_OVH) + LAUNCH
+
+
+# round 2: the large-shape plan is 64x64 tiles at two CTAs per SM (waves of 296 tiles),
+# calibrated on the measured 16384^3 kernel (237.7 ms = 222 waves)
+R_CTA64 = 64 * 64 * 16384 * 2 / (237.7e-3 / 222)
+
+
+def gemm_t64(M, N, K):
+    tiles = math.ceil(M / 64) * math.ceil(N / 64)
+    return math.ceil(tiles / (2 * S)) * (64 * 64 * K * 2 / R_CTA64 + 3e-6) + 4e-6
 
 
 def simulate(K, plan):
@@ -79,7 +89,19 @@ def schedule(M, N, K, R0, Ra, cb0, cb, Rp, Rlast, nlast):
 
 
 def main():
+    global gemm_t
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
+    if "--r02" in sys.argv:     # the round-2 kernel's wave model and a finer geometry grid
+        gemm_t = gemm_t64
+        t, idle = simulate(n, schedule(n, n, n, 3072, 768, 1024, 1536, 3840, 256, 2))
+        print(f"implemented  {t * 1e3:7.2f} ms  {2 * n ** 3 / t / 1e12:6.2f} TFLOP/s  GPU idle {idle * 1e3:5.2f} ms"
+              f"  (kernel alone {gemm_t(n, n, n) * 1e3:.1f} ms)")
+        best = min((simulate(n, schedule(n, n, n, 64 * r0, 64 * ra, 64 * c0, 64 * cbt, 64 * rp, 64 * rl, 2))[0],
+                    r0, ra, c0, cbt, rp, rl)
+                   for r0 in (32, 37, 40, 44, 48, 52, 56) for ra in (4, 8, 12, 16) for c0 in (4, 8, 16, 24)
+                   for cbt in (16, 24, 32, 37, 48) for rp in (37, 48, 60, 74) for rl in (4, 8))
+        print(f"grid best    {best[0] * 1e3:7.2f} ms  (R0, Ra, cb0, cb, Rp, Rlast in 64-row/col tiles) = {best[1:]}")
+        return
     kern = gemm_t(n, n, n)
     old = schedule(n, n, n, 2304, 2304, 2048, 2048, 2048, 2048, 2)      # round-1 first schedule
     new = schedule(n, n, n, 3072, 768, 1024, 1536, 3840, 256, 2)        # host_api.cu now
