@@ -177,7 +177,9 @@ GEMM_API int gemm_num_cfgs(void);
 /* Writes a NUL-terminated name such as "tma_128x128x16_w64x32_s4" into buf. */
 GEMM_API int gemm_cfg_name(int cfg_id, char *buf, int len);
 GEMM_API int gemm_cfg_info(int cfg_id, gemm_cfg_desc *out);
-/* The configuration the heuristic picks for this shape / alignment. */
+/* The configuration the heuristic picks for this shape / alignment (for large operands that
+ * miss the TMA rules -- 2MNK >= 4e9, M, N >= 64, K >= 16 -- the TMA plan the call launches on
+ * its repacked copies; gemm_plan / gemm_plan_ex likewise). */
 GEMM_API int gemm_cfg_select(int64_t M, int64_t N, int64_t K, const double *A, int64_t lda,
                     const double *B, int64_t ldb);
 

@@ -885,8 +885,16 @@ int gemm_cfg_info(int cfg_id, gemm_cfg_desc *out) {
     return GEMM_OK;
 }
 
+// The TMA key a heuristic call on these operands plans with: TMA-eligible operands, or large
+// ones that gemm_impl repacks into aligned rows (it then launches the TMA plan).
+static bool plans_tma(int64_t M, int64_t N, int64_t K, const double *A, int64_t lda, const double *B, int64_t ldb) {
+    if (M == 1) lda += (lda & 1);
+    if (K == 1) ldb += (ldb & 1);
+    return tma_ok(A, lda, B, ldb) || repack_eligible(M, N, K);
+}
+
 int gemm_cfg_select(int64_t M, int64_t N, int64_t K, const double *A, int64_t lda, const double *B, int64_t ldb) {
-    return select_cfg(M, N, K, tma_ok(A, lda, B, ldb));
+    return select_cfg(M, N, K, plans_tma(M, N, K, A, lda, B, ldb));
 }
 
 int gemm_plan_set(int64_t M, int64_t N, int64_t K, int tma, int cfg_id, int splits) {
@@ -977,9 +985,7 @@ int gemm_plan(int64_t M, int64_t N, int64_t K, const double *A, int64_t lda, con
               int *cfg_id, int *splits) {
     clear_error();
     if (!cfg_id || !splits) return set_error(GEMM_ERR_ARG, "cfg_id / splits is NULL");
-    if (M == 1) lda += (lda & 1);
-    if (K == 1) ldb += (ldb & 1);
-    const Choice c = choose(M, N, K, tma_ok(A, lda, B, ldb));
+    const Choice c = choose(M, N, K, plans_tma(M, N, K, A, lda, B, ldb));
     *cfg_id = c.id;
     *splits = c.splits;
     return GEMM_OK;
@@ -989,9 +995,7 @@ int gemm_plan_ex(int64_t M, int64_t N, int64_t K, const double *A, int64_t lda, 
                  int one_pass, int *cfg_id, int *splits) {
     clear_error();
     if (!cfg_id || !splits) return set_error(GEMM_ERR_ARG, "cfg_id / splits is NULL");
-    if (M == 1) lda += (lda & 1);
-    if (K == 1) ldb += (ldb & 1);
-    const Choice c = choose(M, N, K, tma_ok(A, lda, B, ldb), one_pass != 0);
+    const Choice c = choose(M, N, K, plans_tma(M, N, K, A, lda, B, ldb), one_pass != 0);
     *cfg_id = c.id;
     *splits = one_pass ? 1 : c.splits;
     return GEMM_OK;

@@ -123,9 +123,14 @@ def test_heuristic_selection(G):
     pinned = [t[4] for t in table if t[:3] == ["16384", "16384", "16384"]]
     assert pinned and big["name"] == pinned[0]
     odd = G.cfg_info(G.cfg_select(1000, 1000, 1001, 0, 1001, 0, 1000))
-    assert odd["tma"] == 0       # odd lda -> not TMA-eligible
-    mis = G.cfg_info(G.cfg_select(4096, 4096, 4096, 8, 4096, 0, 4096))
+    assert odd["tma"] == 0       # odd lda -> not TMA-eligible (2MNK < 4e9: not repacked)
+    mis = G.cfg_info(G.cfg_select(512, 512, 512, 8, 512, 0, 512))
     assert mis["tma"] == 0       # 8-byte (not 16-byte) aligned A
+    # large operands that miss the TMA rules are repacked by the call, which then launches the
+    # TMA plan of the shape: that is the plan reported
+    big_mis = G.cfg_info(G.cfg_select(4096, 4096, 4096, 8, 4096, 0, 4096))
+    assert big_mis["tma"] == 1
+    assert G.plan(4096, 4096, 4096, 8, 4096, 0, 4096) == G.plan(4096, 4096, 4096, 0, 4096, 0, 4096)
 
 
 @pytest.mark.parametrize("args,needle", [

@@ -43,7 +43,8 @@ def _table_shapes():
 
 
 GRID = [(n, n, n) for n in range(1024, 20481, 1024)]
-SHAPES = sorted(set(_table_shapes()) | set(GRID), key=lambda s: (s[0] * s[1] * s[2], s))
+RECT = [(10000, 9999, 7001)]   # the ragged row of the rectangular sweep (odd K and N: the repack path)
+SHAPES = sorted(set(_table_shapes()) | set(GRID) | set(RECT), key=lambda s: (s[0] * s[1] * s[2], s))
 
 
 def _gen(mode, seed, mat, rows, cols, col0=0, ncols=None):
