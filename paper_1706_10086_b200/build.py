@@ -66,6 +66,8 @@ def up_to_date(lib: str = LIB) -> bool:
 def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
     lib_out, build_dir = (TRACE_LIB, TRACE_BUILD) if trace else (LIB, BUILD)
     if not force and up_to_date(lib_out):
+        if not trace:
+            build_fast(verbose=verbose)
         return lib_out
     os.makedirs(build_dir, exist_ok=True)
     nccl_inc, nccl_lib = _nccl_dirs()
@@ -95,7 +97,35 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
     os.replace(tmp, lib_out)
     if verbose:
         print(f"built {lib_out}")
+    if not trace:
+        build_fast(force=force, verbose=verbose)
     return lib_out
+
+
+def fast_ext_path() -> str:
+    import sysconfig
+    return os.path.join(HERE, "_gemm_fast" + (sysconfig.get_config_var("EXT_SUFFIX") or ".so"))
+
+
+def build_fast(force: bool = False, verbose: bool = False):
+    """The binding's vectorcall entry (csrc/pyfast.c, argument marshalling only); skipped when
+    Python's headers are missing (the binding then calls the same symbol through ctypes)."""
+    import sysconfig
+    src, out = os.path.join(CSRC, "pyfast.c"), fast_ext_path()
+    inc = sysconfig.get_paths()["include"]
+    if not os.path.exists(os.path.join(inc, "Python.h")):
+        return None
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= os.path.getmtime(src):
+        return out
+    tmp = out + ".tmp"
+    cmd = [os.environ.get("CC", "gcc"), "-O2", "-shared", "-fPIC", "-Wall", "-I", inc, src, "-o", tmp]
+    p = subprocess.run(cmd, capture_output=True, text=True)
+    if p.returncode != 0:
+        raise RuntimeError(f"pyfast build failed:\n{p.stderr}")
+    os.replace(tmp, out)
+    if verbose:
+        print(f"built {out}")
+    return out
 
 
 if __name__ == "__main__":

@@ -94,6 +94,17 @@ def _load():
 
 _lib = _load()
 
+# The vectorcall entry (csrc/pyfast.c): the same gemm_f64_ex symbol of this very library,
+# called without ctypes' per-argument conversion; absent -> ctypes.
+try:
+    if os.environ.get("GEMM_NO_FAST"):   # A/B of the host cost (tools/binding_overhead.py)
+        raise ImportError("GEMM_NO_FAST set")
+    from . import _gemm_fast as _fastmod
+    _fastmod.set_target(ctypes.cast(_lib.gemm_f64_ex, ctypes.c_void_p).value)
+    _FAST = _fastmod.gemm_f64_ex
+except ImportError:
+    _FAST = None
+
 # The tuned plan table shipped with the package (produced on a B200 by
 # `python -m paper_1706_10086_b200.tuner`); pinned plans override the size model for
 # exactly these shapes.  Set GEMM_F64_NO_TUNED=1 to use the model alone.
@@ -216,7 +227,10 @@ def gemm(A, B, C, alpha: float = 1.0, beta: float = 0.0, cfg: int | None = None,
     if K2 != K or M2 != M or N2 != N:
         raise ValueError(f"shape mismatch A{tuple(A.shape)} B{tuple(B.shape)} C{tuple(C.shape)}")
     st = _stream_ptr(stream, _on_current_device(A, B, C))
-    if cfg is None and splits is None:
+    if _FAST is not None:   # gemm_f64_ex(cfg -1, splits 0) is gemm_f64_stream; (cfg, 0) is gemm_f64_cfg
+        rc = _FAST(M, N, K, float(alpha), pa, lda, pb, ldb, float(beta), pc, ldc,
+                   -1 if cfg is None else int(cfg), 0 if splits is None else int(splits), st)
+    elif cfg is None and splits is None:
         rc = _lib.gemm_f64_stream(M, N, K, float(alpha), pa, lda, pb, ldb, float(beta), pc, ldc, st)
     elif splits is None:
         rc = _lib.gemm_f64_cfg(M, N, K, float(alpha), pa, lda, pb, ldb, float(beta), pc, ldc, int(cfg), st)

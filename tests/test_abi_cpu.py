@@ -248,3 +248,25 @@ def test_forced_splits_without_tma_is_rejected_explicitly(G):
     lib = G.lib()
     rc = lib.gemm_f64_ex(8, 8, 7, 1.0, 16, 7, 1024, 8, 0.0, 4096, 8, -1, 4, None)
     assert rc == G.GEMM_ERR_UNSUPPORTED and "splits=4" in G.last_error(), G.last_error()
+
+
+def test_fast_entry_calls_the_same_library(G):
+    """The vectorcall entry (csrc/pyfast.c) is built and calls gemm_f64_ex of the library
+    ctypes loaded (one copy: same status codes and the same thread-local error message)."""
+    import ctypes
+    import sysconfig
+    if not os.path.exists(os.path.join(sysconfig.get_paths()["include"], "Python.h")):
+        pytest.skip("no Python headers: the binding uses ctypes")
+    assert G._FAST is not None
+    args_bad = (-1, 64, 64, 1.0, 16, 64, 16, 64, 0.0, 16, 64, -1, 0, None)
+    assert G._FAST(*args_bad) == G.GEMM_ERR_ARG and "M=-1" in G.last_error()
+    assert G._lib.gemm_f64_ex(*args_bad) == G.GEMM_ERR_ARG and "M=-1" in G.last_error()
+    G._lib.gemm_last_error()          # same thread-local error state: set by one, read by the other
+    assert G._FAST(0, 64, 64, 1.0, 16, 64, 16, 64, 0.0, 16, 64, -1, 0, None) == G.GEMM_OK   # M = 0: no-op
+    assert G.last_error() == ""
+    assert G._FAST(4, 4, 8, 1.0, 16, 4, 16, 4, 0.0, 16, 4, -1, 0, None) == G.GEMM_ERR_ARG
+    assert "lda=4" in G.last_error()  # the message the C library wrote
+    with pytest.raises(TypeError):
+        G._FAST(1, 2, 3)
+    addr = ctypes.cast(G._lib.gemm_f64_ex, ctypes.c_void_p).value
+    assert addr
