@@ -12,6 +12,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/gemm_f64.h"
@@ -87,6 +88,97 @@ int64_t best_factor(int64_t fixed, int64_t lo, int64_t hi, int S) {
     }
     return best;
 }
+
+// Block geometry of the schedule above (rows / columns).
+struct Geo {
+    int64_t R0, Ra, cb0, cb, Rp, Rlast;
+    int nlast;
+};
+
+// Copy/compute simulation of the schedule (tools/e2e_sim.py --r02 is the same model): three
+// in-order streams; a GEMM block starts when its copies have landed and the previous block is
+// done, and takes ceil(tiles / (2 SMs)) waves of 64x64 tiles at the calibrated per-CTA rate
+// (16384^3: 222 waves in 237.7 ms) + fixed costs; copies run at the measured pinned PCIe rates.
+// Predicted 251.1 ms at 16384^3 (measured 250.8-252.0) and 38.7 ms for config 4 (38.5).
+constexpr double kRateCta = 64.0 * 64.0 * 16384.0 * 2.0 / (237.7e-3 / 222.0);
+constexpr double kD2H = 53e9;
+
+double sim_gemm(int64_t m, int64_t n, int64_t K, int S) {
+    const int64_t tiles = ((m + 63) / 64) * ((n + 63) / 64);
+    return (double)((tiles + 2 * S - 1) / (2 * S)) * (64.0 * 64.0 * (double)K * 2.0 / kRateCta + 3e-6) + 4e-6;
+}
+
+double simulate(int64_t M, int64_t N, int64_t K, bool c_in, const Geo &g, int S) {
+    double th = 0.0, tc = 0.0, td = 0.0;
+    auto h2d = [&](double bytes) { th += bytes / kH2D; return th; };
+    auto block = [&](double ready, int64_t nr, int64_t nc) {
+        tc = std::max(tc, ready) + sim_gemm(nr, nc, K, S);
+        td = std::max(td, tc) + 8.0 * (double)nr * (double)nc / kD2H;
+    };
+    const double row_bytes = 8.0 * (double)(K + (c_in ? N : 0));
+    const int64_t R0 = std::min(M, g.R0), Ra = std::min(R0, g.Ra);
+    double ready = h2d(row_bytes * (double)Ra);
+    bool first = true;
+    for (int64_t c0 = 0; c0 < N;) {
+        const int64_t nc = std::min(N - c0, first ? g.cb0 : g.cb);
+        ready = h2d(8.0 * (double)K * (double)nc);
+        if (first && Ra < R0) {
+            block(ready, Ra, nc);
+            ready = h2d(row_bytes * (double)(R0 - Ra));
+            block(ready, R0 - Ra, nc);
+        } else {
+            block(ready, R0, nc);
+        }
+        first = false;
+        c0 += nc;
+    }
+    for (int64_t r0 = R0; r0 < M;) {
+        const int64_t rem = M - r0;
+        const int64_t nr = (rem <= g.Rlast || g.Rlast == 0) ? rem : (rem <= g.Rlast + g.Rp ? rem - g.Rlast : g.Rp);
+        ready = h2d(row_bytes * (double)nr);
+        const bool last = (r0 + nr >= M);
+        const int64_t lcb = last ? std::max<int64_t>(kTn, ((N + g.nlast - 1) / g.nlast + kTn - 1) / kTn * kTn) : N;
+        for (int64_t c0 = 0; c0 < N; c0 += lcb) block(ready, nr, std::min(N, c0 + lcb) - c0);
+        r0 += nr;
+    }
+    return std::max(tc, td);
+}
+
+// The geometry for this shape: the wave-fill rule's (round 1), unless a coarse grid of
+// alternatives simulates more than 1 % faster -- e.g. config 4 (32768 x 4096 x 4096), where the
+// rule's 5888-row panels leave the device->host copies of C unoverlapped (38.7 -> 34.0 ms
+// predicted).  Cached per shape; the search costs ~1 ms once.
+Geo plan_geometry(int64_t M, int64_t N, int64_t K, bool c_in, int S, const Geo &rule) {
+    static std::mutex mu;
+    static std::map<std::tuple<int64_t, int64_t, int64_t, bool, int>, Geo> cache;
+    const auto key = std::make_tuple(M, N, K, c_in, S);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+    }
+    Geo best = rule;
+    const double t_rule = simulate(M, N, K, c_in, rule, S);
+    double t_best = t_rule;
+    for (int64_t r0 : {16, 32, 48})
+        for (int64_t ra : {4, 12, 16})
+            for (int64_t cbt : {16, 24})
+                for (int64_t rp : {16, 32, 48, 60, 92})
+                    for (int64_t rl : {2, 4})
+                        for (int nl : {1, 2}) {
+                            const Geo g{64 * r0, 64 * ra, 64 * 16, 64 * cbt, 64 * rp, 64 * rl, nl};
+                            const double t = simulate(M, N, K, c_in, g, S);
+                            if (t < t_best) {
+                                t_best = t;
+                                best = g;
+                            }
+                        }
+    if (t_best > 0.99 * t_rule) best = rule;
+    std::lock_guard<std::mutex> lk(mu);
+    if (cache.size() > 256) cache.clear();
+    cache[key] = best;
+    return best;
+}
 }  // namespace
 
 static int host_impl(int64_t M, int64_t N, int64_t K, double alpha, const double *A, int64_t lda, const double *B,
@@ -132,6 +224,14 @@ static int host_impl(int64_t M, int64_t N, int64_t K, double alpha, const double
         Rp = best_factor(tn_all, 8, 24, S) * kTm;                                // 15 x 256 at N = 16384
         Rlast = kTm;
         nlast = N >= 2 * 512 ? 2 : 1;
+        const Geo g = plan_geometry(M, N, K, need_c_in, S, Geo{R0, Ra, cb0, cb, Rp, Rlast, (int)nlast});
+        R0 = std::min(M, g.R0);
+        Ra = std::min(R0, g.Ra);
+        cb0 = std::min(N, g.cb0);
+        cb = std::min(N, g.cb);
+        Rp = g.Rp;
+        Rlast = g.Rlast;
+        nlast = g.nlast;
     }
     // column blocks of panel 0: cb0, then cb each
     std::vector<std::pair<int64_t, int64_t>> cols;

@@ -537,6 +537,23 @@ def test_host_entry_point_large_pinned(cuda_lib):
     assert r.ok, str(r)
 
 
+def test_host_entry_point_searched_geometry(cuda_lib):
+    """A shape whose block geometry comes from the copy/compute simulation's search rather than
+    the wave-fill rule (8192 x 4096 x 4096: 1024-row panels, one-block thin last panel): the
+    result is still bitwise the one-pass device call's, and within the bound."""
+    M, N, K = 8192, 4096, 4096
+    A, B, C0 = synth.problem(M, N, K, seed=19)
+    tA = torch.from_numpy(A).pin_memory()
+    tB = torch.from_numpy(B).pin_memory()
+    tC = torch.from_numpy(C0.copy()).pin_memory()
+    cuda_lib.gemm_host(tA, tB, tC, 1.5, 0.5)
+    assert np.array_equal(tC.numpy(), run_gpu(cuda_lib, A, B, C0, 1.5, 0.5, splits=1))
+    rows = _rows(M, extra=4)
+    ref, mag = oracle.dgemm(1.5, A[rows], B, 0.5, C0[rows], want_mag=True)
+    r = oracle.check(tC.numpy()[rows], ref, oracle.bound(K, 1.5, 0.5, mag, C0[rows]))
+    assert r.ok, str(r)
+
+
 def test_host_entry_point_pipelined_odd_padded(cuda_lib):
     """The blocked copy/compute pipeline (row panel 0 by column blocks, later row panels,
     last panel by column blocks) on an odd shape with padded host leading dimensions."""
