@@ -67,7 +67,8 @@ static int ensure_events(std::vector<cudaEvent_t> &v, size_t n) {
 // Block widths and panel heights are chosen so that each GEMM's 256x64 tile count falls
 // just below a multiple of the SM count (little partial-wave waste).  The geometry was
 // chosen with a copy/compute simulation calibrated on measured PCIe and GEMM rates
-// (DESIGN.md §e2e): 16384^3 264 -> 255 ms.
+// (DESIGN.md §e2e): 16384^3 264 -> 255 ms.  Round 2: the same simulation runs here per shape
+// (plan_geometry) and replaces the rule's geometry when a coarse grid finds one > 1 % faster.
 namespace {
 constexpr double kRate = 36.6e12;   // FP64 DMMA GEMM rate (FLOP/s)
 constexpr double kH2D = 55e9;       // pinned H2D bandwidth (B/s), PCIe 5 x16
