@@ -149,6 +149,16 @@ GEMM_API int gemm_f64_host(int64_t M, int64_t N, int64_t K, double alpha,
                   const double *A, int64_t lda, const double *B, int64_t ldb,
                   double beta, double *C, int64_t ldc);
 
+/* The block schedule gemm_f64_host uses for this shape (introspection, tests, tools): writes
+ * geometry[7] = {R0 first row panel, Ra its first block's rows, cb0 first column block, cb
+ * later column blocks, Rp later row panels, Rlast thin last panel (0: none), nlast its column
+ * blocks} (caller-owned) and, if sim_seconds != NULL, the copy/compute simulation's predicted
+ * seconds for it (tools/e2e_sim.py --r02 is the same model).  num_sms <= 0: the current
+ * device's SM count.  Host-only arithmetic, no device work.  Negative sizes or NULL geometry
+ * -> GEMM_ERR_ARG. */
+GEMM_API int gemm_host_plan(int64_t M, int64_t N, int64_t K, int beta_nonzero, int num_sms,
+                   int64_t geometry[7], double *sim_seconds);
+
 /* Release the device buffers cached by gemm_f64_host on the current device. */
 GEMM_API int gemm_host_pool_release(void);
 

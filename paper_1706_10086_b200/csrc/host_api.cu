@@ -180,6 +180,25 @@ Geo plan_geometry(int64_t M, int64_t N, int64_t K, bool c_in, int S, const Geo &
     cache[key] = best;
     return best;
 }
+// The block geometry of one gemm_f64_host call: one shot for tiny problems (< ~1 ms of GPU
+// work), else the wave-fill rule's geometry or the simulated search's (plan_geometry).
+Geo host_geometry(int64_t M, int64_t N, int64_t K, bool need_ab, bool need_c_in, int S) {
+    const double flops = 2.0 * (double)M * (double)N * (double)K;
+    if (!need_ab || flops < 2e10) return Geo{M, M, N, N, M, 0, 1};
+    const int64_t tn_all = (N + kTn - 1) / kTn;
+    const int64_t r_bal = (int64_t)(4.0 * kRate / kH2D / kTm) + 1;          // 11 tile rows
+    const int64_t r0 = best_factor(std::min<int64_t>(tn_all, 24), r_bal, r_bal + 2, S);
+    const int64_t R0 = std::min<int64_t>(M, r0 * kTm);
+    const int64_t cbt = best_factor(r0, 16, 32, S);                          // 24 at S = 148
+    const Geo rule{R0, std::min<int64_t>(R0, 3 * kTm), std::min<int64_t>(N, 16 * kTn), std::min<int64_t>(N, cbt * kTn),
+                   best_factor(tn_all, 8, 24, S) * kTm /* 15 x 256 at N = 16384 */, kTm, N >= 2 * 512 ? 2 : 1};
+    Geo g = plan_geometry(M, N, K, need_c_in, S, rule);
+    g.R0 = std::min(M, g.R0);
+    g.Ra = std::min(g.R0, g.Ra);
+    g.cb0 = std::min(N, g.cb0);
+    g.cb = std::min(N, g.cb);
+    return g;
+}
 }  // namespace
 
 static int host_impl(int64_t M, int64_t N, int64_t K, double alpha, const double *A, int64_t lda, const double *B,
@@ -210,30 +229,9 @@ static int host_impl(int64_t M, int64_t N, int64_t K, double alpha, const double
     if ((rc = ensure(&P.dC, &P.nC, (size_t)M * N))) return rc;
 
     // ---- geometry
-    const double flops = 2.0 * (double)M * (double)N * (double)K;
-    const bool tiny = !need_ab || flops < 2e10;      // < ~1 ms of GPU work: one shot
-    const int64_t tn_all = (N + kTn - 1) / kTn;
-    int64_t R0 = M, Ra = M, Rp = M, Rlast = 0, cb0 = N, cb = N, nlast = 1;
-    if (!tiny) {
-        const int64_t r_bal = (int64_t)(4.0 * kRate / kH2D / kTm) + 1;          // 11 tile rows
-        const int64_t r0 = best_factor(std::min<int64_t>(tn_all, 24), r_bal, r_bal + 2, S);
-        R0 = std::min<int64_t>(M, r0 * kTm);
-        Ra = std::min<int64_t>(R0, 3 * kTm);
-        const int64_t cbt = best_factor(r0, 16, 32, S);                          // 24 at S = 148
-        cb = std::min<int64_t>(N, cbt * kTn);
-        cb0 = std::min<int64_t>(N, 16 * kTn);
-        Rp = best_factor(tn_all, 8, 24, S) * kTm;                                // 15 x 256 at N = 16384
-        Rlast = kTm;
-        nlast = N >= 2 * 512 ? 2 : 1;
-        const Geo g = plan_geometry(M, N, K, need_c_in, S, Geo{R0, Ra, cb0, cb, Rp, Rlast, (int)nlast});
-        R0 = std::min(M, g.R0);
-        Ra = std::min(R0, g.Ra);
-        cb0 = std::min(N, g.cb0);
-        cb = std::min(N, g.cb);
-        Rp = g.Rp;
-        Rlast = g.Rlast;
-        nlast = g.nlast;
-    }
+    const Geo geo = host_geometry(M, N, K, need_ab, need_c_in, S);
+    const int64_t R0 = geo.R0, Ra = geo.Ra, Rp = geo.Rp, Rlast = geo.Rlast, cb0 = geo.cb0, cb = geo.cb;
+    const int64_t nlast = geo.nlast;
     // column blocks of panel 0: cb0, then cb each
     std::vector<std::pair<int64_t, int64_t>> cols;
     for (int64_t c0 = 0; c0 < N;) {
@@ -352,6 +350,25 @@ extern "C" {
 int gemm_f64_host(int64_t M, int64_t N, int64_t K, double alpha, const double *A, int64_t lda, const double *B,
                   int64_t ldb, double beta, double *C, int64_t ldc) {
     return host_impl(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+}
+
+int gemm_host_plan(int64_t M, int64_t N, int64_t K, int beta_nonzero, int num_sms, int64_t geometry[7],
+                   double *sim_seconds) {
+    clear_error();
+    if (M < 0 || N < 0 || K < 0) return set_error(GEMM_ERR_ARG, "negative shape");
+    if (!geometry) return set_error(GEMM_ERR_ARG, "geometry is NULL");
+    int S = num_sms;
+    if (S <= 0) {
+        int dev = 0;
+        int rc = cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+        if (!rc) rc = cuda_check(cudaDeviceGetAttribute(&S, cudaDevAttrMultiProcessorCount, dev), "SM count");
+        if (rc) return rc;
+    }
+    const Geo g = host_geometry(M, N, K, M > 0 && N > 0 && K > 0, beta_nonzero != 0, S);
+    const int64_t v[7] = {g.R0, g.Ra, g.cb0, g.cb, g.Rp, g.Rlast, g.nlast};
+    for (int i = 0; i < 7; ++i) geometry[i] = v[i];
+    if (sim_seconds) *sim_seconds = simulate(M, N, K, beta_nonzero != 0, g, S);
+    return GEMM_OK;
 }
 
 int gemm_host_pool_release(void) {

@@ -23,7 +23,7 @@ FILL_MODES = {"uniform": 0, "dyadic": 1, "int8": 2, "ones": 3, "identity": 4, "z
 
 # every symbol include/gemm_f64.h declares (tests check the library exports them all)
 EXPORTS = ("gemm_f64", "gemm_f64_stream", "gemm_f64_cfg", "gemm_f64_ex", "gemm_f32", "gemm_f32_stream",
-           "gemm_f32_cfg", "gemm_f32_num_cfgs", "gemm_f32_cfg_name", "gemm_f64_host", "gemm_host_pool_release",
+           "gemm_f32_cfg", "gemm_f32_num_cfgs", "gemm_f32_cfg_name", "gemm_f64_host", "gemm_host_plan", "gemm_host_pool_release",
            "gemm_workspace_release",
            "gemm_num_cfgs", "gemm_cfg_name", "gemm_cfg_info", "gemm_cfg_select", "gemm_plan", "gemm_plan_ex", "gemm_plan_set",
            "gemm_plan_clear", "gemm_tune_load", "gemm_tune_save", "gemm_plan_autotune", "gemm_last_error",
@@ -61,6 +61,7 @@ def _load():
         "gemm_f32_cfg_name": (ci, [ci, ctypes.c_char_p, ci]),
         "gemm_f64_host": (ci, core),
         "gemm_host_pool_release": (ci, []),
+        "gemm_host_plan": (ci, [i64, i64, i64, ci, ci, ctypes.POINTER(i64), ctypes.POINTER(dbl)]),
         "gemm_workspace_release": (ci, []),
         "gemm_num_cfgs": (ci, []),
         "gemm_cfg_name": (ci, [ci, ctypes.c_char_p, ci]),
@@ -299,6 +300,15 @@ def gemm_host(A, B, C, alpha: float = 1.0, beta: float = 0.0):
         raise ValueError("shape mismatch")
     _check(_lib.gemm_f64_host(M, N, K, float(alpha), pa, lda, pb, ldb, float(beta), pc, ldc))
     return C
+
+
+def host_plan(M: int, N: int, K: int, beta_nonzero: bool = False, num_sms: int = 0) -> tuple:
+    """gemm_f64_host's block schedule for this shape: (dict of R0, Ra, cb0, cb, Rp, Rlast, nlast;
+    the simulation's predicted seconds)."""
+    g = (ctypes.c_int64 * 7)()
+    sec = ctypes.c_double()
+    _check(_lib.gemm_host_plan(M, N, K, int(bool(beta_nonzero)), int(num_sms), g, ctypes.byref(sec)))
+    return dict(zip(("R0", "Ra", "cb0", "cb", "Rp", "Rlast", "nlast"), list(g))), sec.value
 
 
 def host_pool_release():
