@@ -230,7 +230,7 @@ GEMM_API int gemm_tune_save(const char *path, int *n_saved);
  * the better model score) is pinned as by gemm_plan_set and written to *cfg_id / *splits, its
  * device seconds per call to *seconds (may be NULL).  Synchronous; A and B are only read.
  * Candidates: the plan in force, each of the `top` best-scored configurations at its
- * best-scored slice count, and slice counts S - 1, S + 1, 2S of the three best-scored ones;
+ * best-scored slice count, and slice counts 1, S - 1, S + 1, 2S of the three best-scored ones;
  * each costs about 5 calls of the shape.  Operands that miss the TMA rules (alignment, odd
  * leading dimension) are timed on packed copies when the problem is large enough for the
  * heuristic call to repack them (2MNK >= 4e9, M, N >= 64, K >= 16), which then launches the

@@ -1065,9 +1065,10 @@ int gemm_plan_autotune(int64_t M, int64_t N, int64_t K, const double *A, int64_t
     }
 
     // candidates: the plan in force; each of the `top` best-scored configurations at its
-    // best-scored slice count; the neighbouring slice counts (S - 1, S + 1, 2S) of the three
-    // best-scored configurations (the model ranks configurations better than slice counts:
-    // profiles/r02/regret_small_seed29_auto8.csv)
+    // best-scored slice count; the one-pass plan and the neighbouring slice counts (1, S - 1,
+    // S + 1, 2S) of the three best-scored configurations (the model ranks configurations better
+    // than slice counts: profiles/r02/regret_small_seed29_auto8.csv; without S = 1 a 360x345x310
+    // shape kept 32x32 x3, 16 % behind 32x32 x1, regret_small_seed47_m4.csv)
     std::vector<Choice> cands{cur};
     {
         std::vector<Scored> v;
@@ -1088,7 +1089,7 @@ int gemm_plan_autotune(int64_t M, int64_t N, int64_t K, const double *A, int64_t
         };
         for (size_t i = 0; i < per_cfg.size() && (int)i < top; ++i) add(per_cfg[i].id, per_cfg[i].splits);
         for (size_t i = 0; i < per_cfg.size() && i < 3; ++i)
-            for (int S : {per_cfg[i].splits - 1, per_cfg[i].splits + 1, 2 * per_cfg[i].splits})
+            for (int S : {1, per_cfg[i].splits - 1, per_cfg[i].splits + 1, 2 * per_cfg[i].splits})
                 for (const Scored &x : v)
                     if (x.id == per_cfg[i].id && x.splits == S) add(x.id, S);
     }
